@@ -1,0 +1,69 @@
+// Internal declarations shared by the libswb.so translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/swb.h"
+
+// int32 sentinel for minus infinity on the device (the reference uses
+// -(2**61) in int64, kernels.py:14).  Drift from the sentinel is bounded by
+// swb_check_range(): sentinel-derived values stay below SWB_NEG_REPORT and
+// real values stay above it.
+#define SWB_NEG32 (-(1 << 30))
+
+struct swb_seq {
+  uint8_t* fwd = nullptr;  // device, n codes
+  uint8_t* rev = nullptr;  // device, reversed copy
+  int64_t n = 0;
+  bool live = false;
+};
+
+// A grow-only device scratch buffer.
+struct swb_buf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+struct swb_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::mutex mu;
+  std::vector<swb_seq> seqs;
+  int sms = 0;
+  double last_kernel_ms = 0.0;
+  int64_t launches = 0;
+  int max_ctas_per_sm = 0;  // 0 = occupancy limit
+  int force_R = 0;          // 0 = pick rows-per-lane from the pass height
+  // scratch
+  swb_buf jobs, rowbuf, progress, results, finals, misc, host_pinned;
+};
+
+void swb_set_error(const char* fmt, ...);
+int swb_fail(int code, const char* fmt, ...);
+void* swb_scratch(swb_buf& b, size_t bytes);  // device; nullptr on failure
+void* swb_scratch_host(swb_buf& b, size_t bytes);
+
+#define SWB_CUDA(call)                                                           \
+  do {                                                                           \
+    cudaError_t _e = (call);                                                     \
+    if (_e != cudaSuccess)                                                       \
+      return swb_fail(SWB_ECUDA, "%s failed: %s (%s:%d)", #call,                 \
+                      cudaGetErrorString(_e), __FILE__, __LINE__);               \
+  } while (0)
+
+#define SWB_API_BEGIN(ctx)                                                       \
+  if ((ctx) == nullptr) return swb_fail(SWB_EINVAL, "null context");             \
+  std::lock_guard<std::mutex> _swb_lock((ctx)->mu);                              \
+  {                                                                              \
+    cudaError_t _se = cudaSetDevice((ctx)->device);                              \
+    if (_se != cudaSuccess)                                                      \
+      return swb_fail(SWB_ECUDA, "cudaSetDevice: %s", cudaGetErrorString(_se));  \
+  }
+
+#define SWB_API_END() return SWB_OK

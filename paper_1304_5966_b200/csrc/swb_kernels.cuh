@@ -1,0 +1,452 @@
+// Device code of the SW# wavefront pass (B200, sm_100a).
+//
+// One persistent kernel replaces WavefrontEngine.run_wavefront (engine.py:188-282)
+// together with kernels.affine_block (kernels.py:21-88).
+//
+// Decomposition:
+//   * A *warp-strip* is 32 lanes x R rows of seq1.  Lane l owns rows
+//     [R0 + l*R, R0 + (l+1)*R) and keeps their H and E in registers; it sweeps the
+//     strip's column range one column per step.  Lane l processes column s - l at
+//     step s, so the vertical dependency (H, F of the row above) arrives from lane
+//     l-1 by one __shfl_up per value per step, and the diagonal is the value that
+//     arrived one step earlier.
+//   * Warp-strips are chained through global memory: the strip's bottom row
+//     (H, F) is flushed every 32 steps to a row buffer, followed by a release
+//     store of the strip's progress counter; the strip below acquires it.  Two
+//     row buffers per pass suffice (ordering argument in DESIGN.md §3.3).
+//   * Work items are (pass, strip) pairs claimed in order by an atomic counter,
+//     so any number of independent passes (Myers-Miller levels, the two halves
+//     of split mode) share one launch; a strip only waits on an item claimed
+//     before it, so the persistent launch cannot deadlock.
+//
+// Cell update (all int32, DPX; H kept as hm = H - (go+ge), E plain, F plain):
+//   h2 = max(diag_m + (s + go + ge), E [, 0])        VIADDMNMX(.RELU)
+//   F  = max(F - ge, h2_above - go - ge)              VIADDMNMX  (1-op F chain)
+//   hm = max(F - (go+ge), h2 - (go+ge)) = H - (go+ge) IADD + VIADDMNMX
+//   E' = max(E - ge, hm)                              VIADDMNMX
+// F may use the pre-F value h2 of the row above instead of H because
+// F - (go+ge) <= F - ge (go >= 0): max(F - ge, max(h2, F) - go - ge) ==
+// max(F - ge, h2 - go - ge).  The substitution score s + go + ge is one PRMT
+// (sign-replicating byte select) from a per-column profile word.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "swb_internal.h"
+
+namespace swb {
+
+constexpr int kTrackNone = 0;
+constexpr int kTrackMin = 1;
+constexpr int kTrackMax = 2;
+constexpr int kPadCode = 7;  // row code for padding rows (profile byte -128)
+
+struct JobDev {
+  const uint8_t* rows;  // code of row i = rows[i * rstep]
+  const uint8_t* cols;  // code of column j = cols[j * cstep]
+  int32_t rstep, cstep;
+  int32_t n1, n2;
+  int32_t border;
+  int32_t fill_h;  // H written into skipped cells: 0 (local) or NEG
+  int32_t has_band, band_lo, band_hi;
+  int32_t prune;
+  int32_t nstrips;
+  int32_t want_final;
+  int64_t item_base;
+  int2* buf[2];          // row buffers (hm, F), n2 entries each
+  int32_t* progress;     // per strip: columns < progress[s] of strip s are published
+  int32_t* fin_h;        // final row H (DP columns 1..n2) or null
+  int32_t* fin_f;
+  int4* strip_res;       // per strip (score_m, i, j, has)
+  unsigned long long* counters;  // [0] cells, [1] blocks executed, [2] blocks pruned
+  int32_t* prune_best;   // running best score (plain) for pruning
+};
+
+struct PassParams {
+  const JobDev* jobs;
+  int32_t njobs;
+  int32_t pad0;
+  int64_t total_items;
+  unsigned long long* claim;
+  int32_t goe, ge, max_sub;
+  uint32_t tlo[8], thi[8];  // profile word per column code
+};
+
+__device__ __forceinline__ int vmaxadd(int a, int b, int c) { return __viaddmax_s32(a, b, c); }
+
+__device__ __forceinline__ uint32_t prmt(uint32_t lo, uint32_t hi, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(lo), "r"(hi), "r"(sel));
+  return d;
+}
+
+__device__ __forceinline__ int ld_acquire(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release(int32_t* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ int ld_relaxed(const int32_t* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Border values, engine.py:340-401.  I is a DP row, J a DP column.
+__device__ __forceinline__ int left_h(int border, int I, int go, int ge) {
+  switch (border) {
+    case SWB_BORDER_LOCAL: return 0;
+    case SWB_BORDER_RESTRICTED: return I == 0 ? 0 : SWB_NEG32;
+    case SWB_BORDER_GLOBAL_FREE: return I == 0 ? 0 : -go - I * ge;
+    case SWB_BORDER_GLOBAL_CONTINUE: return I == 0 ? SWB_NEG32 : -I * ge;
+    default: return I == 0 ? SWB_NEG32 : -go - I * ge;  // charge
+  }
+}
+
+__device__ __forceinline__ int top_h(int border, int J, int go, int ge) {
+  switch (border) {
+    case SWB_BORDER_LOCAL: return 0;
+    case SWB_BORDER_RESTRICTED: return J == 0 ? 0 : SWB_NEG32;
+    case SWB_BORDER_GLOBAL_FREE: return J == 0 ? 0 : -go - J * ge;
+    default: return SWB_NEG32;  // continue / charge: origin blocked, no top row
+  }
+}
+
+// Column range of strip s: all columns, or the band's admissible columns for
+// the strip's rows (cells outside are skipped with the fill values, as the
+// reference does for banded-out blocks, engine.py:225-231, :286-293).
+template <int R>
+__device__ __forceinline__ void strip_range(const JobDev& J, int s, int& cb, int& ce) {
+  if (!J.has_band) {
+    cb = 0;
+    ce = J.n2;
+    return;
+  }
+  const int r0 = s * 32 * R;
+  int r1 = r0 + 32 * R - 1;
+  if (r1 > J.n1 - 1) r1 = J.n1 - 1;
+  long long lo = (long long)r0 - J.band_hi;
+  long long hi = (long long)r1 - J.band_lo + 1;
+  if (lo < 0) lo = 0;
+  if (hi > J.n2) hi = J.n2;
+  if (hi < lo) hi = lo;
+  cb = (int)lo;
+  ce = (int)hi;
+}
+
+struct WarpSmem {
+  int4 ring[64];  // per column c: (top hm, top F, profile lo, profile hi) at [c & 63]
+  int2 out[32];   // lane-31 outputs of the current 32-step block
+};
+
+template <int R, bool LOCAL, int TRACK, bool FINAL>
+__device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, int s,
+                                       WarpSmem* sm, const uint32_t* __restrict__ tlo_s,
+                                       const uint32_t* __restrict__ thi_s) {
+  const JobDev J = Jg;
+  const int lane = threadIdx.x & 31;
+  const int goe = P.goe, ge = P.ge;
+  const int go = goe - ge;
+  const int n1 = J.n1, n2 = J.n2;
+  const int R0 = s * 32 * R;
+  const int lrow0 = R0 + lane * R;
+  int nvalid = n1 - lrow0;
+  nvalid = nvalid < 0 ? 0 : (nvalid > R ? R : nvalid);
+  const int fillm = J.fill_h - goe;
+
+  int cb, ce;
+  strip_range<R>(J, s, cb, ce);
+  int cbp = 0, cep = 0;
+  if (s > 0) strip_range<R>(J, s - 1, cbp, cep);
+  const int2* __restrict__ inbuf = J.buf[(s + 1) & 1];  // written by strip s-1
+  int2* __restrict__ outbuf = J.buf[s & 1];
+  int32_t* my_progress = J.progress + s;
+  const int32_t* up_progress = s > 0 ? J.progress + (s - 1) : nullptr;
+
+  if (cb >= ce) {
+    if (lane == 0) {
+      st_release(my_progress, 0x7fffffff);
+      J.strip_res[s] = make_int4(0, -1, -1, 0);
+    }
+    return;
+  }
+
+  // Row codes -> PRMT selectors (byte a, sign replicated into bytes 1..3).
+  uint32_t sel[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = lrow0 + r;
+    uint32_t a = (i < n1) ? (uint32_t)J.rows[(long long)i * J.rstep] : (uint32_t)kPadCode;
+    sel[r] = a | ((a | 8u) << 4) | ((a | 8u) << 8) | ((a | 8u) << 12);
+  }
+
+  // Left state at column cb (E holds the value for the column about to run).
+  int H[R], E[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int hl = (cb == 0) ? left_h(J.border, lrow0 + r + 1, go, ge) - goe : fillm;
+    H[r] = hl;
+    E[r] = vmaxadd(SWB_NEG32, -ge, hl);
+  }
+  // Diagonal for row 0 at column cb: H(lrow0 - 1, cb - 1).
+  int diag;
+  if (cb == 0) {
+    diag = left_h(J.border, lrow0, go, ge) - goe;
+  } else if (lane != 0) {
+    diag = fillm;
+  } else if (s == 0) {
+    diag = top_h(J.border, cb, go, ge) - goe;
+  } else if (cb - 1 >= cbp && cb - 1 < cep) {
+    while (ld_acquire(up_progress) < cb) __nanosleep(32);
+    diag = __ldcg(inbuf + (cb - 1)).x;
+  } else {
+    diag = fillm;
+  }
+
+  // Tracking state (kernels.py:73-84): best in the hm frame.
+  int best = (TRACK == kTrackMin) ? -goe : INT32_MIN;
+  int thr = (TRACK == kTrackMin) ? -goe + 1 : INT32_MIN;
+  int bi = -1, bj = -1;
+
+  int rstar = 0, lstar = -1;
+  if (FINAL) {
+    const int off = n1 - 1 - R0;
+    lstar = off / R;
+    rstar = off % R;
+  }
+
+  int out_hm = fillm, out_f = SWB_NEG32;
+  long long pruned_blocks = 0, exec_blocks = 0;
+  const int s_end = ce + 31;
+
+  for (int s0 = cb; s0 < s_end; s0 += 32) {
+    // (1) stage lane-0 inputs and profile words for columns [s0, s0 + 32).
+    {
+      const int c = s0 + lane;
+      if (s > 0 && s0 < cep && s0 + 32 > cbp) {
+        const int need = (s0 + 32 < cep) ? s0 + 32 : cep;
+        while (ld_acquire(up_progress) < need) __nanosleep(64);
+      }
+      if (c < ce) {
+        int th, tf;
+        if (s == 0) {
+          th = top_h(J.border, c + 1, go, ge) - goe;
+          tf = SWB_NEG32;
+        } else if (c >= cbp && c < cep) {
+          int2 v = __ldcg(inbuf + c);
+          th = v.x;
+          tf = v.y;
+        } else {
+          th = fillm;
+          tf = SWB_NEG32;
+        }
+        const int code = J.cols[(long long)c * J.cstep];
+        sm->ring[c & 63] = make_int4(th, tf, (int)tlo_s[code], (int)thi_s[code]);
+      }
+      __syncwarp();
+    }
+
+    // (2) pruning: skip the whole 32-step block when no path through it can
+    // reach the running best (phase1.py:24-41, :55-59; strict inequality).
+    bool skip = false;
+    if (LOCAL && J.prune && s0 - 31 >= cb && s0 + 32 <= ce) {
+      int m = out_hm > diag ? out_hm : diag;
+#pragma unroll
+      for (int r = 0; r < R; ++r) m = m > H[r] ? m : H[r];
+      const int tv = sm->ring[(s0 + lane) & 63].x;
+      m = m > tv ? m : tv;
+      m = __reduce_max_sync(0xffffffffu, m);
+      const int inmax = m + goe > 0 ? m + goe : 0;
+      const int rem_r = n1 - R0;
+      const int rem_c = n2 - (s0 - 31);
+      const long long bound =
+          (long long)inmax + (long long)P.max_sub * (long long)(rem_r < rem_c ? rem_r : rem_c);
+      const int pb = ld_relaxed(J.prune_best);
+      skip = bound < (long long)pb;
+    }
+
+    if (skip) {
+      ++pruned_blocks;
+      const int negE = vmaxadd(SWB_NEG32, -ge, -goe);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        H[r] = -goe;
+        E[r] = negE;
+      }
+      diag = (lane == 0) ? sm->ring[(s0 + 31) & 63].x : -goe;
+      out_hm = -goe;
+      out_f = SWB_NEG32;
+      sm->out[lane] = make_int2(-goe, SWB_NEG32);
+      __syncwarp();
+    } else {
+      ++exec_blocks;
+      // (3) 32 steps.
+#pragma unroll 1
+      for (int k = 0; k < 32; ++k) {
+        const int step = s0 + k;
+        const int col = step - lane;
+        const int4 rv = sm->ring[col & 63];
+        int up_h = __shfl_up_sync(0xffffffffu, out_hm, 1);
+        int up_f = __shfl_up_sync(0xffffffffu, out_f, 1);
+        if (lane == 0) {
+          up_h = rv.x;
+          up_f = rv.y;
+        }
+        if (col >= cb && col < ce) {
+          const uint32_t tl = (uint32_t)rv.z, th = (uint32_t)rv.w;
+          int d = diag;
+          diag = up_h;
+          int fv = up_f;
+          int hab = up_h;  // (H or pre-F H) of the row above, minus go+ge
+          int cm = INT32_MIN;
+          int fh = 0, ff = 0;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const int sv = (int)prmt(tl, th, sel[r]);
+            const int h2 = LOCAL ? __viaddmax_s32_relu(d, sv, E[r]) : __viaddmax_s32(d, sv, E[r]);
+            fv = vmaxadd(fv, -ge, hab);
+            const int h2m = h2 - goe;
+            const int hm = vmaxadd(fv, -goe, h2m);
+            E[r] = vmaxadd(E[r], -ge, hm);
+            d = H[r];
+            H[r] = hm;
+            hab = h2m;
+            if (TRACK != kTrackNone) {
+              if (r & 1) cm = __vimax3_s32(cm, H[r - 1], hm);
+              else if (r == R - 1) cm = cm > hm ? cm : hm;
+            }
+            if (FINAL && r == rstar) {
+              fh = hm;
+              ff = fv;
+            }
+          }
+          out_hm = H[R - 1];
+          out_f = fv;
+          if (TRACK != kTrackNone) {
+            if (cm >= thr) {
+              // slow path: exact lexicographic update (kernels.py:73-84)
+#pragma unroll
+              for (int r = 0; r < R; ++r) {
+                const int v = H[r];
+                const int i = lrow0 + r;
+                bool upd;
+                if (TRACK == kTrackMin)
+                  upd = (r < nvalid) && v > -goe && (v > best || (v == best && i < bi));
+                else
+                  upd = (r < nvalid) && (v > best || (v == best && i >= bi));
+                if (upd) {
+                  best = v;
+                  bi = i;
+                  bj = col;
+                }
+              }
+              if (TRACK == kTrackMin) thr = best > -goe ? best : -goe + 1;
+              else thr = best;
+            }
+          }
+          if (FINAL && lane == lstar) {
+            J.fin_h[col] = fh + goe;
+            J.fin_f[col] = ff;
+          }
+          if (lane == 31) sm->out[k] = make_int2(out_hm, out_f);
+        }
+      }
+      __syncwarp();
+    }
+
+    // (4) flush lane-31 outputs for columns [s0 - 31, s0 + 1) and publish.
+    {
+      const int c = s0 - 31 + lane;
+      if (c >= cb && c < ce) __stcg(outbuf + c, sm->out[lane]);
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) {
+        int pub = s0 + 1;
+        if (pub > ce) pub = ce;
+        if (pub >= cb) st_release(my_progress, pub);
+      }
+    }
+
+    // (5) running best for pruning (monotone, never ahead of the truth).
+    if (LOCAL && J.prune && TRACK == kTrackMin) {
+      const int bm = __reduce_max_sync(0xffffffffu, best);
+      if (lane == 0 && bm > -goe) atomicMax(J.prune_best, bm + goe);
+    }
+  }
+  if (lane == 0) st_release(my_progress, ce);
+
+  // Strip result: warp reduction with the mode's tie rule (engine.py:247-259).
+  if (TRACK != kTrackNone) {
+    int b = best, ii = bi, jj = bj;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const int ob = __shfl_down_sync(0xffffffffu, b, o);
+      const int oi = __shfl_down_sync(0xffffffffu, ii, o);
+      const int oj = __shfl_down_sync(0xffffffffu, jj, o);
+      bool take;
+      if (oi < 0) take = false;
+      else if (ii < 0) take = true;
+      else if (TRACK == kTrackMin)
+        take = ob > b || (ob == b && (oi < ii || (oi == ii && oj < jj)));
+      else
+        take = ob > b || (ob == b && (oi > ii || (oi == ii && oj > jj)));
+      if (take) {
+        b = ob;
+        ii = oi;
+        jj = oj;
+      }
+    }
+    if (lane == 0) J.strip_res[s] = make_int4(b, ii, jj, ii >= 0 ? 1 : 0);
+  } else if (lane == 0) {
+    J.strip_res[s] = make_int4(0, -1, -1, 0);
+  }
+  if (lane == 0) {
+    int rows_here = n1 - R0;
+    if (rows_here > 32 * R) rows_here = 32 * R;
+    const long long cells =
+        (long long)(ce - cb) * rows_here - pruned_blocks * 32LL * rows_here;
+    atomicAdd(&J.counters[0], (unsigned long long)(cells > 0 ? cells : 0));
+    atomicAdd(&J.counters[1], (unsigned long long)exec_blocks);
+    atomicAdd(&J.counters[2], (unsigned long long)pruned_blocks);
+  }
+}
+
+template <int R, bool LOCAL, int TRACK>
+__global__ void __launch_bounds__(128) pass_kernel(const PassParams P) {
+  __shared__ WarpSmem wsm[4];
+  __shared__ uint32_t tlo_s[8], thi_s[8];
+  if (threadIdx.x < 8) {
+    tlo_s[threadIdx.x] = P.tlo[threadIdx.x];
+    thi_s[threadIdx.x] = P.thi[threadIdx.x];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  WarpSmem* sm = &wsm[warp];
+  for (;;) {
+    long long item = 0;
+    if (lane == 0) item = (long long)atomicAdd(P.claim, 1ULL);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= P.total_items) break;
+    // locate the pass owning this item (jobs sorted by item_base)
+    int lo = 0, hi = P.njobs - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (P.jobs[mid].item_base <= item) lo = mid;
+      else hi = mid - 1;
+    }
+    const JobDev& J = P.jobs[lo];
+    const int s = (int)(item - J.item_base);
+    if (J.want_final && s == J.nstrips - 1)
+      run_strip<R, LOCAL, TRACK, true>(P, J, s, sm, tlo_s, thi_s);
+    else
+      run_strip<R, LOCAL, TRACK, false>(P, J, s, sm, tlo_s, thi_s);
+  }
+}
+
+}  // namespace swb

@@ -1,0 +1,444 @@
+// Host side of the wavefront pass: PassSpec -> device jobs -> one persistent
+// launch per (recurrence, tracking, rows-per-lane) class -> PassResult.
+// Replaces WavefrontEngine.run_wavefront (engine.py:188-282).
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "swb_kernels.cuh"
+#include "swb_passes.h"
+
+using namespace swb;
+
+__global__ void fill2_kernel(int32_t* a, int32_t va, int32_t* b, int32_t vb, int64_t n) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    a[x] = va;
+    b[x] = vb;
+  }
+}
+
+int swb_prepare_scheme(const swb_scheme* s, SchemeInt* out) {
+  if (!s) return swb_fail(SWB_EINVAL, "null scheme");
+  if (s->k < 1 || s->k > 7)
+    return swb_fail(SWB_EUNSUPPORTED, "alphabet size %d not supported (1..7)", s->k);
+  if (s->gap_open < 0 || s->gap_extend < 1)
+    return swb_fail(SWB_EINVAL, "gap_open must be >= 0 and gap_extend >= 1");
+  const int goe = s->gap_open + s->gap_extend;
+  int mx = INT32_MIN;
+  for (int a = 0; a < s->k; ++a)
+    for (int b = 0; b < s->k; ++b) mx = std::max(mx, s->sub[a * s->k + b]);
+  out->goe = goe;
+  out->ge = s->gap_extend;
+  out->go = s->gap_open;
+  out->k = s->k;
+  out->max_sub = mx;
+  if (mx != s->max_sub)
+    return swb_fail(SWB_EINVAL, "max_sub %d does not match the matrix maximum %d", s->max_sub, mx);
+  for (int b = 0; b < 8; ++b) {
+    uint8_t bytes[8];
+    for (int a = 0; a < 8; ++a) {
+      int v = -128;
+      if (a < s->k && b < s->k) {
+        v = s->sub[a * s->k + b] + goe;
+        if (v < -127 || v > 127)
+          return swb_fail(SWB_EUNSUPPORTED,
+                          "substitution %d + gap_open + gap_extend %d does not fit the int8 profile",
+                          s->sub[a * s->k + b], goe);
+      }
+      bytes[a] = (uint8_t)(int8_t)v;
+    }
+    memcpy(&out->tlo[b], bytes, 4);
+    memcpy(&out->thi[b], bytes + 4, 4);
+  }
+  return SWB_OK;
+}
+
+int swb_check_range(const SchemeInt& sc, long long n1, long long n2) {
+  // Real DP values lie in [-D, D]; sentinel-derived ones in NEG32 +- D.  Keep both
+  // inside their half of the int32 range (see SWB_NEG_REPORT).
+  const long long D = (long long)sc.ge * (n1 + n2) + 2LL * sc.goe +
+                      (long long)std::max(sc.max_sub, 0) * std::min(n1, n2) + 1024;
+  if (D >= (1LL << 28))
+    return swb_fail(SWB_ERANGE,
+                    "pass %lld x %lld with gap_extend %d / max_sub %d exceeds the int32 "
+                    "dynamic range of the device kernels",
+                    n1, n2, sc.ge, sc.max_sub);
+  return SWB_OK;
+}
+
+int swb_resolve_seq(swb_ctx* ctx, int32_t id, int64_t off, int64_t len, int32_t rev,
+                    const uint8_t** base, int* step) {
+  if (id < 0 || id >= (int32_t)ctx->seqs.size() || !ctx->seqs[id].live)
+    return swb_fail(SWB_EINVAL, "bad sequence id %d", id);
+  const swb_seq& s = ctx->seqs[id];
+  if (off < 0 || len < 0 || off + len > s.n)
+    return swb_fail(SWB_EINVAL, "slice [%lld, %lld) outside sequence of length %lld",
+                    (long long)off, (long long)(off + len), (long long)s.n);
+  if (!rev) {
+    *base = s.fwd + off;
+    *step = 1;
+  } else {
+    // row r reads code[off + len - 1 - r] == rev[n - off - len + r]
+    *base = s.rev + (s.n - off - len);
+    *step = 1;
+  }
+  return SWB_OK;
+}
+
+namespace {
+
+int pick_rows_per_lane(int n1) {
+  if (n1 >= 2048) return 32;
+  if (n1 >= 256) return 8;
+  return 2;
+}
+
+template <int R, bool LOCAL, int TRACK>
+int launch_kernel(swb_ctx* ctx, const PassParams& P, long long items, int max_ctas_per_sm) {
+  auto kern = pass_kernel<R, LOCAL, TRACK>;
+  int per_sm = 0;
+  SWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, 0));
+  if (per_sm < 1) return swb_fail(SWB_ECUDA, "pass kernel does not fit on an SM");
+  if (max_ctas_per_sm > 0 && per_sm > max_ctas_per_sm) per_sm = max_ctas_per_sm;
+  long long cap = (long long)per_sm * ctx->sms;
+  long long need = (items + 3) / 4;
+  int grid = (int)std::min(cap, std::max(need, 1LL));
+  kern<<<grid, 128, 0, ctx->stream>>>(P);
+  ctx->launches++;
+  SWB_CUDA(cudaGetLastError());
+  return SWB_OK;
+}
+
+template <int R>
+int launch_dispatch(swb_ctx* ctx, const PassParams& P, long long items, bool local, int track) {
+  const int cap = ctx->max_ctas_per_sm;
+  if (local) {
+    if (track == kTrackMin) return launch_kernel<R, true, kTrackMin>(ctx, P, items, cap);
+    return swb_fail(SWB_EUNSUPPORTED, "local passes support TRACK_MIN only");
+  }
+  if (track == kTrackNone) return launch_kernel<R, false, kTrackNone>(ctx, P, items, cap);
+  if (track == kTrackMin) return launch_kernel<R, false, kTrackMin>(ctx, P, items, cap);
+  return launch_kernel<R, false, kTrackMax>(ctx, P, items, cap);
+}
+
+struct Arena {
+  char* base = nullptr;
+  size_t off = 0;
+  template <typename T>
+  T* take(size_t count) {
+    off = (off + 255) & ~(size_t)255;
+    T* p = reinterpret_cast<T*>(base + off);
+    off += sizeof(T) * std::max<size_t>(count, 1);
+    return p;
+  }
+};
+
+}  // namespace
+
+int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs,
+                   double* kernel_ms_total) {
+  if (kernel_ms_total) *kernel_ms_total = 0.0;
+  // group: (local, track, R)
+  std::vector<int> order(reqs.size());
+  for (size_t q = 0; q < reqs.size(); ++q) {
+    order[q] = (int)q;
+    PassReq& r = reqs[q];
+    if (r.n1 < 1 || r.n2 < 1) return swb_fail(SWB_EINVAL, "cannot tile an empty matrix");
+    int rc = swb_check_range(sc, r.n1, r.n2);
+    if (rc) return rc;
+    r.R = r.force_R ? r.force_R : pick_rows_per_lane(r.n1);
+  }
+  auto key = [&](int q) {
+    const PassReq& r = reqs[q];
+    return (r.local ? 1000 : 0) + r.track * 100 + r.R;
+  };
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return key(a) < key(b); });
+
+  size_t g0 = 0;
+  while (g0 < order.size()) {
+    size_t g1 = g0;
+    while (g1 < order.size() && key(order[g1]) == key(order[g0])) ++g1;
+    const PassReq& head = reqs[order[g0]];
+    const int R = head.R;
+    const int nj = (int)(g1 - g0);
+
+    // layout
+    long long total_strips = 0, total_cols = 0, final_cols = 0;
+    for (size_t t = g0; t < g1; ++t) {
+      PassReq& r = reqs[order[t]];
+      r.nstrips = (int)((r.n1 + 32LL * R - 1) / (32LL * R));
+      total_strips += r.nstrips;
+      total_cols += r.n2;
+      if (r.want_final && r.fin_h_dev == nullptr) final_cols += r.n2;
+    }
+    size_t bytes = 256 * 8 + sizeof(JobDev) * nj + sizeof(int32_t) * total_strips +
+                   sizeof(unsigned long long) * 3 * nj + sizeof(int32_t) * nj + 64 +
+                   sizeof(int4) * total_strips + sizeof(int2) * 2 * total_cols +
+                   sizeof(int32_t) * 2 * final_cols + 4096 + 256 * 8 * (size_t)nj;
+    Arena A;
+    A.base = (char*)swb_scratch(ctx->rowbuf, bytes);
+    if (!A.base) return swb_fail(SWB_ECUDA, "out of device memory (%zu bytes of pass scratch)", bytes);
+    JobDev* d_jobs = A.take<JobDev>(nj);
+    // zeroed region
+    size_t zero_begin = (A.off + 255) & ~(size_t)255;
+    int32_t* d_prog = A.take<int32_t>(total_strips);
+    unsigned long long* d_cnt = A.take<unsigned long long>(3 * nj);
+    int32_t* d_pbest = A.take<int32_t>(nj);
+    unsigned long long* d_claim = A.take<unsigned long long>(1);
+    size_t zero_end = A.off;
+    int4* d_res = A.take<int4>(total_strips);
+    // host staging (pinned)
+    size_t hbytes = sizeof(JobDev) * nj + sizeof(int4) * total_strips +
+                    sizeof(unsigned long long) * 3 * nj + 1024;
+    char* hbase = (char*)swb_scratch_host(ctx->host_pinned, hbytes);
+    if (!hbase) return swb_fail(SWB_ECUDA, "pinned host allocation failed");
+    JobDev* h_jobs = reinterpret_cast<JobDev*>(hbase);
+    int4* h_res = reinterpret_cast<int4*>(hbase + sizeof(JobDev) * nj);
+    unsigned long long* h_cnt =
+        reinterpret_cast<unsigned long long*>(hbase + sizeof(JobDev) * nj + sizeof(int4) * total_strips);
+
+    long long item = 0, strip_off = 0;
+    for (int t = 0; t < nj; ++t) {
+      PassReq& r = reqs[order[g0 + t]];
+      JobDev& J = h_jobs[t];
+      memset(&J, 0, sizeof(J));
+      J.rows = r.rows;
+      J.rstep = r.rstep;
+      J.cols = r.cols;
+      J.cstep = r.cstep;
+      J.n1 = r.n1;
+      J.n2 = r.n2;
+      J.border = r.border;
+      J.fill_h = r.local ? 0 : SWB_NEG32;
+      J.has_band = r.has_band ? 1 : 0;
+      if (r.has_band) {
+        long long lo = std::max<long long>(r.band_lo, -(1LL << 30));
+        long long hi = std::min<long long>(r.band_hi, (1LL << 30));
+        J.band_lo = (int32_t)lo;
+        J.band_hi = (int32_t)hi;
+      }
+      J.prune = r.prune ? 1 : 0;
+      J.nstrips = r.nstrips;
+      J.want_final = r.want_final ? 1 : 0;
+      J.item_base = item;
+      J.buf[0] = A.take<int2>(r.n2);
+      J.buf[1] = A.take<int2>(r.n2);
+      J.progress = d_prog + strip_off;
+      J.strip_res = d_res + strip_off;
+      J.counters = d_cnt + 3 * t;
+      J.prune_best = d_pbest + t;
+      if (r.want_final) {
+        if (r.fin_h_dev) {
+          J.fin_h = r.fin_h_dev;
+          J.fin_f = r.fin_f_dev;
+        } else {
+          J.fin_h = A.take<int32_t>(r.n2);
+          J.fin_f = A.take<int32_t>(r.n2);
+          r.fin_h_dev = J.fin_h;
+          r.fin_f_dev = J.fin_f;
+        }
+      }
+      r.res_offset = strip_off;
+      item += r.nstrips;
+      strip_off += r.nstrips;
+    }
+    if (A.off > bytes) return swb_fail(SWB_ECUDA, "internal: pass arena overflow");
+
+    SWB_CUDA(cudaMemcpyAsync(d_jobs, h_jobs, sizeof(JobDev) * nj, cudaMemcpyHostToDevice, ctx->stream));
+    SWB_CUDA(cudaMemsetAsync(A.base + zero_begin, 0, zero_end - zero_begin, ctx->stream));
+    for (int t = 0; t < nj; ++t) {
+      const PassReq& r = reqs[order[g0 + t]];
+      if (r.want_final) {
+        int blocks = (int)std::min<long long>((r.n2 + 255) / 256, 2048);
+        fill2_kernel<<<blocks, 256, 0, ctx->stream>>>(r.fin_h_dev, h_jobs[t].fill_h, r.fin_f_dev,
+                                                     SWB_NEG32, r.n2);
+        ctx->launches++;
+      }
+    }
+    SWB_CUDA(cudaGetLastError());
+
+    PassParams P;
+    memset(&P, 0, sizeof(P));
+    P.jobs = d_jobs;
+    P.njobs = nj;
+    P.total_items = item;
+    P.claim = d_claim;
+    P.goe = sc.goe;
+    P.ge = sc.ge;
+    P.max_sub = sc.max_sub;
+    memcpy(P.tlo, sc.tlo, sizeof(P.tlo));
+    memcpy(P.thi, sc.thi, sizeof(P.thi));
+
+    SWB_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+    int rc;
+    if (R == 32) rc = launch_dispatch<32>(ctx, P, item, head.local, head.track);
+    else if (R == 8) rc = launch_dispatch<8>(ctx, P, item, head.local, head.track);
+    else rc = launch_dispatch<2>(ctx, P, item, head.local, head.track);
+    if (rc) return rc;
+    SWB_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+    SWB_CUDA(cudaMemcpyAsync(h_res, d_res, sizeof(int4) * total_strips, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    SWB_CUDA(cudaMemcpyAsync(h_cnt, d_cnt, sizeof(unsigned long long) * 3 * nj,
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    SWB_CUDA(cudaStreamSynchronize(ctx->stream));
+    float ms = 0.f;
+    SWB_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    ctx->last_kernel_ms = ms;
+    if (kernel_ms_total) *kernel_ms_total += ms;
+
+    for (int t = 0; t < nj; ++t) {
+      PassReq& r = reqs[order[g0 + t]];
+      r.kernel_ms = ms;
+      long long bs = 0, bi = -1, bj = -1;
+      bool have = false;
+      for (int q = 0; q < r.nstrips; ++q) {
+        const int4 v = h_res[r.res_offset + q];
+        if (!v.w) continue;
+        const long long s = (long long)v.x + sc.goe, i = v.y, j = v.z;
+        bool take;
+        if (!have) take = true;
+        else if (r.track == kTrackMin)
+          take = s > bs || (s == bs && (i < bi || (i == bi && j < bj)));
+        else
+          take = s > bs || (s == bs && (i > bi || (i == bi && j > bj)));
+        if (take) {
+          bs = s;
+          bi = i;
+          bj = j;
+          have = true;
+        }
+      }
+      if (r.track == kTrackMin) {
+        if (!have || bs <= 0) {
+          bs = 0;
+          bi = bj = -1;
+        }
+      } else if (r.track == kTrackNone || !have) {
+        bs = SWB_NEG_INF_REF;
+        bi = bj = -1;
+      } else if (bs < SWB_NEG_REPORT) {
+        bs = SWB_NEG_INF_REF + (bs - (long long)SWB_NEG32);
+      }
+      r.best_score = bs;
+      r.best_i = bi;
+      r.best_j = bj;
+      r.cells = (long long)h_cnt[3 * t + 0];
+      r.blocks_exec = (long long)h_cnt[3 * t + 1];
+      r.blocks_pruned = (long long)h_cnt[3 * t + 2];
+      r.blocks_total = (long long)r.nstrips * ((r.n2 + 31) / 32);
+    }
+    g0 = g1;
+  }
+  return SWB_OK;
+}
+
+static inline long long left_h_host(int border, long long I, int go, int ge) {
+  switch (border) {
+    case SWB_BORDER_LOCAL: return 0;
+    case SWB_BORDER_RESTRICTED: return I == 0 ? 0 : SWB_NEG_INF_REF;
+    case SWB_BORDER_GLOBAL_FREE: return I == 0 ? 0 : -go - I * ge;
+    case SWB_BORDER_GLOBAL_CONTINUE: return I == 0 ? SWB_NEG_INF_REF : -I * ge;
+    default: return I == 0 ? SWB_NEG_INF_REF : -go - I * ge;
+  }
+}
+
+static inline long long left_f_host(int border, long long I, int go, int ge) {
+  switch (border) {
+    case SWB_BORDER_LOCAL:
+    case SWB_BORDER_RESTRICTED: return SWB_NEG_INF_REF;
+    case SWB_BORDER_GLOBAL_FREE: return I == 0 ? SWB_NEG_INF_REF : -go - I * ge;
+    case SWB_BORDER_GLOBAL_CONTINUE: return I == 0 ? 0 : -I * ge;
+    default: return I == 0 ? -(long long)go : -go - I * ge;
+  }
+}
+
+static inline long long widen(int32_t v) {
+  if ((long long)v < SWB_NEG_REPORT) return SWB_NEG_INF_REF + ((long long)v - (long long)SWB_NEG32);
+  return v;
+}
+
+extern "C" int32_t swb_set_option(swb_ctx* ctx, const char* name, int64_t value) {
+  if (!ctx || !name) return swb_fail(SWB_EINVAL, "bad arguments");
+  if (!strcmp(name, "max_ctas_per_sm")) {
+    ctx->max_ctas_per_sm = (int)value;
+    return SWB_OK;
+  }
+  if (!strcmp(name, "rows_per_lane")) {
+    if (value != 0 && value != 2 && value != 8 && value != 32)
+      return swb_fail(SWB_EINVAL, "rows_per_lane must be 0 (auto), 2, 8 or 32");
+    ctx->force_R = (int)value;
+    return SWB_OK;
+  }
+  return swb_fail(SWB_EINVAL, "unknown option %s", name);
+}
+
+extern "C" int32_t swb_pass(swb_ctx* ctx, const swb_scheme* scheme, const swb_pass_desc* descs,
+                            int32_t n, swb_pass_out* outs) {
+  SWB_API_BEGIN(ctx);
+  if (n < 0 || (n > 0 && (!descs || !outs))) return swb_fail(SWB_EINVAL, "bad arguments");
+  SchemeInt sc;
+  int rc = swb_prepare_scheme(scheme, &sc);
+  if (rc) return rc;
+  std::vector<PassReq> reqs(n);
+  for (int q = 0; q < n; ++q) {
+    const swb_pass_desc& d = descs[q];
+    PassReq& r = reqs[q];
+    rc = swb_resolve_seq(ctx, d.seq1, d.off1, d.len1, d.rev1, &r.rows, &r.rstep);
+    if (rc) return rc;
+    rc = swb_resolve_seq(ctx, d.seq2, d.off2, d.len2, d.rev2, &r.cols, &r.cstep);
+    if (rc) return rc;
+    r.n1 = (int)d.len1;
+    r.n2 = (int)d.len2;
+    if (d.border < SWB_BORDER_LOCAL || d.border > SWB_BORDER_GLOBAL_CHARGE)
+      return swb_fail(SWB_EINVAL, "bad border %d", d.border);
+    if (d.track < 0 || d.track > 2) return swb_fail(SWB_EINVAL, "bad track mode %d", d.track);
+    r.border = d.border;
+    r.local = d.clamp_zero != 0;
+    r.track = d.track;
+    if (r.local && (d.border != SWB_BORDER_LOCAL || d.track != SWB_TRACK_MIN || d.has_band))
+      return swb_fail(SWB_EUNSUPPORTED, "clamped passes must use local borders, TRACK_MIN, no band");
+    if (!r.local && d.prune) return swb_fail(SWB_EUNSUPPORTED, "pruning needs a local pass");
+    r.has_band = d.has_band != 0;
+    r.band_lo = d.band_lo;
+    r.band_hi = d.band_hi;
+    r.prune = d.prune != 0;
+    r.want_final = d.want_final_rows != 0;
+    if (r.want_final && (!d.final_row_h || !d.final_row_f))
+      return swb_fail(SWB_EINVAL, "want_final_rows needs final_row_h/final_row_f");
+    r.force_R = ctx->force_R;
+  }
+  double ms = 0.0;
+  rc = swb_run_passes(ctx, sc, reqs, &ms);
+  if (rc) return rc;
+  for (int q = 0; q < n; ++q) {
+    const swb_pass_desc& d = descs[q];
+    PassReq& r = reqs[q];
+    swb_pass_out& o = outs[q];
+    o.best_score = r.best_score;
+    o.best_i = r.best_i;
+    o.best_j = r.best_j;
+    o.cells_executed = r.cells;
+    o.tiles_total = r.blocks_total;
+    o.tiles_executed = r.blocks_exec;
+    o.tiles_pruned = r.blocks_pruned;
+    o.tiles_banded_out = std::max<long long>(0, r.blocks_total - r.blocks_exec - r.blocks_pruned);
+    o.kernel_ms = r.kernel_ms;
+    if (r.want_final) {
+      std::vector<int32_t> th(r.n2), tf(r.n2);
+      SWB_CUDA(cudaMemcpyAsync(th.data(), r.fin_h_dev, sizeof(int32_t) * r.n2,
+                               cudaMemcpyDeviceToHost, ctx->stream));
+      SWB_CUDA(cudaMemcpyAsync(tf.data(), r.fin_f_dev, sizeof(int32_t) * r.n2,
+                               cudaMemcpyDeviceToHost, ctx->stream));
+      SWB_CUDA(cudaStreamSynchronize(ctx->stream));
+      d.final_row_h[0] = left_h_host(r.border, r.n1, sc.go, sc.ge);
+      d.final_row_f[0] = left_f_host(r.border, r.n1, sc.go, sc.ge);
+      for (int c = 0; c < r.n2; ++c) {
+        d.final_row_h[c + 1] = widen(th[c]);
+        d.final_row_f[c + 1] = widen(tf[c]);
+      }
+    }
+  }
+  SWB_API_END();
+}

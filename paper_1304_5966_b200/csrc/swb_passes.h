@@ -1,0 +1,42 @@
+// Internal pass-request interface shared by swb_pass.cu and swb_mm.cu.
+#pragma once
+
+#include <vector>
+
+#include "swb_internal.h"
+
+struct SchemeInt {
+  int goe, ge, go, max_sub, k;
+  uint32_t tlo[8], thi[8];
+};
+
+struct PassReq {
+  const uint8_t* rows = nullptr;
+  const uint8_t* cols = nullptr;
+  int rstep = 1, cstep = 1;
+  int n1 = 0, n2 = 0;
+  int border = 0;
+  bool local = false;
+  int track = 0;
+  bool has_band = false;
+  long long band_lo = 0, band_hi = 0;
+  bool prune = false;
+  bool want_final = false;
+  int32_t* fin_h_dev = nullptr;  // device int32[n2] (cell columns); allocated if null
+  int32_t* fin_f_dev = nullptr;
+  int force_R = 0;
+  // filled by swb_run_passes
+  int R = 0;
+  int nstrips = 0;
+  long long res_offset = 0;
+  long long best_score = 0, best_i = -1, best_j = -1;
+  long long cells = 0, blocks_exec = 0, blocks_pruned = 0, blocks_total = 0;
+  double kernel_ms = 0.0;
+};
+
+int swb_prepare_scheme(const swb_scheme* s, SchemeInt* out);
+int swb_check_range(const SchemeInt& sc, long long n1, long long n2);
+int swb_resolve_seq(swb_ctx* ctx, int32_t id, int64_t off, int64_t len, int32_t rev,
+                    const uint8_t** base, int* step);
+int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs,
+                   double* kernel_ms_total);

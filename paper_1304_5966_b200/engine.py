@@ -1,0 +1,300 @@
+"""Device context and the pass operator API (replaces engine.py).
+
+`DeviceContext` owns one libswb context (stream, scratch, uploaded
+sequences) per device.  `Session` holds the two uploaded sequences of one
+align()/score_only() call so every pass of every phase addresses slices of
+the same device-resident forward/reversed copies (no per-pass H2D).
+
+`WavefrontEngine.run_wavefront(PassSpec) -> PassResult` is the operator-level
+drop-in for the reference engine (engine.py:143-282): same result fields, with
+the PassSpec callables replaced by the border family / prune flag enums the
+C ABI takes (include/swb.h).
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .errors import DeviceUnavailable
+from .model import ScoringScheme
+
+NEG_INF = _lib.NEG_INF_REF
+TRACK_NONE, TRACK_MIN, TRACK_MAX = _lib.TRACK_NONE, _lib.TRACK_MIN, _lib.TRACK_MAX
+BORDERS = {
+    "local": _lib.BORDER_LOCAL,
+    "restricted": _lib.BORDER_RESTRICTED,
+    "free": _lib.BORDER_FREE,
+    "continue": _lib.BORDER_CONTINUE,
+    "charge": _lib.BORDER_CHARGE,
+}
+# Reference block dims (engine.py:30-31); accepted for API parity, the device
+# tiling is fixed by the kernel (32 lanes x R rows per warp-strip).
+DEFAULT_BLOCK_ROWS = 512
+DEFAULT_BLOCK_COLS = 512
+
+_contexts: dict[int, "DeviceContext"] = {}
+_ctx_lock = threading.Lock()
+
+
+def scheme_struct(scheme: ScoringScheme) -> _lib.Scheme:
+    k = len(scheme.alphabet)
+    if k > 7:
+        raise ValueError(f"alphabets of {k} symbols are not supported on the device (max 7)")
+    s = _lib.Scheme()
+    s.k = k
+    flat = np.asarray(scheme.matrix, dtype=np.int64).reshape(-1)
+    if flat.size and (flat.max() > 2 ** 20 or flat.min() < -(2 ** 20)):
+        raise ValueError("substitution scores out of the supported range")
+    for x, v in enumerate(flat.tolist()):
+        s.sub[x] = int(v)
+    s.gap_open = int(scheme.gap_open)
+    s.gap_extend = int(scheme.gap_extend)
+    s.max_sub = int(flat.max())
+    return s
+
+
+class DeviceContext:
+    def __init__(self, device: int = 0):
+        lib = _lib.load()
+        ptr = lib.swb_ctx_create(int(device))
+        if not ptr:
+            raise DeviceUnavailable(f"cannot create a B200 context on device {device}: "
+                                    f"{_lib.last_error()}")
+        self.lib = lib
+        self.ptr = ptr
+        self.device = int(device)
+        self.lock = threading.Lock()
+
+    # -- sequences -----------------------------------------------------------
+    def upload(self, codes: np.ndarray) -> int:
+        codes = np.ascontiguousarray(codes, dtype=np.uint8)
+        sid = ctypes.c_int32()
+        _lib.check(self.lib.swb_seq_upload(self.ptr, codes.ctypes.data_as(ctypes.c_void_p),
+                                           codes.size, ctypes.byref(sid)), "swb_seq_upload")
+        return int(sid.value)
+
+    def release(self, sid: int) -> None:
+        _lib.check(self.lib.swb_seq_release(self.ptr, int(sid)), "swb_seq_release")
+
+    # -- operators -----------------------------------------------------------
+    def passes(self, scheme: _lib.Scheme, descs: list[_lib.PassDesc]) -> list[_lib.PassOut]:
+        n = len(descs)
+        arr = (_lib.PassDesc * n)(*descs)
+        outs = (_lib.PassOut * n)()
+        _lib.check(self.lib.swb_pass(self.ptr, ctypes.byref(scheme), arr, n, outs), "swb_pass")
+        return list(outs)
+
+    def crossings(self, scheme, s1: int, s2: int, subs: np.ndarray, band: bool):
+        """subs: structured array with _lib.Subproblem layout."""
+        n = int(subs.shape[0])
+        out = (_lib.Crossing * n)()
+        cells = ctypes.c_int64()
+        sub_ptr = subs.ctypes.data_as(ctypes.POINTER(_lib.Subproblem))
+        _lib.check(self.lib.swb_crossings(self.ptr, ctypes.byref(scheme), s1, s2, sub_ptr, n,
+                                          int(band), out, ctypes.byref(cells)), "swb_crossings")
+        res = np.frombuffer(out, dtype=CROSSING_DTYPE, count=n).copy()
+        return res, int(cells.value)
+
+    def leaves(self, scheme, s1: int, s2: int, subs: np.ndarray, band: bool):
+        n = int(subs.shape[0])
+        rows = (subs["ei"] - subs["si"]).astype(np.int64)
+        cols = (subs["ej"] - subs["sj"]).astype(np.int64)
+        cap = rows + cols
+        offsets = np.zeros(n, dtype=np.int64)
+        if n > 1:
+            offsets[1:] = np.cumsum(cap)[:-1]
+        ops = np.empty(int(cap.sum()) + 1, dtype=np.uint8)
+        counts = np.empty(n, dtype=np.int64)
+        scores = np.empty(n, dtype=np.int64)
+        vp = ctypes.c_void_p
+        _lib.check(self.lib.swb_leaves(self.ptr, ctypes.byref(scheme), s1, s2,
+                                       subs.ctypes.data_as(ctypes.POINTER(_lib.Subproblem)), n,
+                                       int(band), ops.ctypes.data_as(vp),
+                                       offsets.ctypes.data_as(vp), counts.ctypes.data_as(vp),
+                                       scores.ctypes.data_as(vp)), "swb_leaves")
+        return ops, offsets, counts, scores
+
+    def measure_int_peak(self) -> dict:
+        p = _lib.IntPeak()
+        _lib.check(self.lib.swb_measure_int_peak(self.ptr, ctypes.byref(p)), "swb_measure_int_peak")
+        return {name: getattr(p, name) for name, _ in _lib.IntPeak._fields_}
+
+    def set_option(self, name: str, value: int) -> None:
+        _lib.check(self.lib.swb_set_option(self.ptr, name.encode(), int(value)), "swb_set_option")
+
+    @property
+    def launch_count(self) -> int:
+        return int(self.lib.swb_launch_count(self.ptr))
+
+    @property
+    def last_kernel_ms(self) -> float:
+        return float(self.lib.swb_last_kernel_ms(self.ptr))
+
+
+SUBPROBLEM_DTYPE = np.dtype([("si", "<i8"), ("sj", "<i8"), ("ei", "<i8"), ("ej", "<i8"),
+                             ("expected", "<i8"), ("start_vgap", "<i4"), ("end_vgap", "<i4")])
+CROSSING_DTYPE = np.dtype([("mid_i", "<i8"), ("mid_j", "<i8"), ("upper", "<i8"),
+                           ("lower", "<i8"), ("gap_join", "<i4"), ("status", "<i4")])
+assert SUBPROBLEM_DTYPE.itemsize == ctypes.sizeof(_lib.Subproblem)
+assert CROSSING_DTYPE.itemsize == ctypes.sizeof(_lib.Crossing)
+
+
+def get_context(device: int = 0) -> DeviceContext:
+    with _ctx_lock:
+        ctx = _contexts.get(device)
+        if ctx is None:
+            ctx = DeviceContext(device)
+            _contexts[device] = ctx
+        return ctx
+
+
+@dataclass
+class PassResult:
+    """engine.PassResult (engine.py:120-131); tiles replace 512x512 blocks."""
+
+    best_score: int
+    best_i: int
+    best_j: int
+    final_row_h: Optional[np.ndarray]
+    final_row_f: Optional[np.ndarray]
+    total_blocks: int
+    executed_blocks: int
+    pruned_blocks: int
+    banded_out_blocks: int
+    cells_executed: int
+    kernel_ms: float = 0.0
+
+
+class Session:
+    """The two sequences of one alignment, resident on one device."""
+
+    def __init__(self, ctx: DeviceContext, codes1: np.ndarray, codes2: np.ndarray,
+                 scheme: ScoringScheme):
+        self.ctx = ctx
+        self.n1 = int(codes1.size)
+        self.n2 = int(codes2.size)
+        self.codes1 = codes1
+        self.codes2 = codes2
+        self.scheme = scheme
+        self.cs = scheme_struct(scheme)
+        self.s1 = ctx.upload(codes1)
+        self.s2 = ctx.upload(codes2)
+        self.kernel_ms = 0.0
+        self.cells = 0
+
+    def close(self):
+        if self.s1 is not None:
+            self.ctx.release(self.s1)
+            self.ctx.release(self.s2)
+            self.s1 = self.s2 = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+        return False
+
+    def desc(self, rows: tuple, cols: tuple, border: str, clamp: bool, track: int,
+             band=None, prune=False, final=None) -> _lib.PassDesc:
+        """rows/cols = (offset, length, reversed) slices of seq1/seq2."""
+        d = _lib.PassDesc()
+        d.seq1, d.seq2 = self.s1, self.s2
+        d.off1, d.len1, d.rev1 = int(rows[0]), int(rows[1]), int(rows[2])
+        d.off2, d.len2, d.rev2 = int(cols[0]), int(cols[1]), int(cols[2])
+        d.border = BORDERS[border]
+        d.clamp_zero = int(clamp)
+        d.track = int(track)
+        if band is not None:
+            d.has_band, d.band_lo, d.band_hi = 1, int(band[0]), int(band[1])
+        d.prune = int(prune)
+        if final is not None:
+            d.want_final_rows = 1
+            d.final_row_h = final[0].ctypes.data
+            d.final_row_f = final[1].ctypes.data
+        return d
+
+    def run(self, specs: list[dict]) -> list[PassResult]:
+        """Run several passes in one device launch; each spec holds the
+        keyword arguments of desc() plus want_final (bool)."""
+        descs, finals = [], []
+        for sp in specs:
+            sp = dict(sp)
+            want = sp.pop("want_final", False)
+            fin = None
+            if want:
+                n2 = int(sp["cols"][1])
+                fin = (np.empty(n2 + 1, dtype=np.int64), np.empty(n2 + 1, dtype=np.int64))
+            finals.append(fin)
+            descs.append(self.desc(final=fin, **sp))
+        outs = self.ctx.passes(self.cs, descs)
+        res = []
+        for o, fin in zip(outs, finals):
+            self.kernel_ms += o.kernel_ms
+            self.cells += o.cells_executed
+            res.append(PassResult(
+                int(o.best_score), int(o.best_i), int(o.best_j),
+                fin[0] if fin else None, fin[1] if fin else None,
+                int(o.tiles_total), int(o.tiles_executed), int(o.tiles_pruned),
+                int(o.tiles_banded_out), int(o.cells_executed), float(o.kernel_ms)))
+        # one launch carries all specs: count its time once
+        if len(outs) > 1:
+            self.kernel_ms -= sum(o.kernel_ms for o in outs[1:])
+        return res
+
+
+@dataclass
+class PassSpec:
+    """Device form of engine.PassSpec (engine.py:93-117): the left_border
+    callable becomes `border`, the prune callable the phase-1 `prune` flag."""
+
+    codes1: np.ndarray
+    codes2: np.ndarray
+    scheme: ScoringScheme
+    border: str = "local"
+    clamp_zero: bool = True
+    track: int = TRACK_MIN
+    band: Optional[tuple[int, int]] = None
+    prune: bool = False
+    want_final_rows: bool = True
+
+
+class WavefrontEngine:
+    """Reference-compatible engine facade (engine.py:143-185).  `workers`,
+    block dims, `meter` and `trace` are accepted for signature parity; the
+    device decomposition is fixed by the kernel."""
+
+    def __init__(self, workers: int = 1, block_rows: int = DEFAULT_BLOCK_ROWS,
+                 block_cols: int = DEFAULT_BLOCK_COLS, meter=None, trace=None, device: int = 0):
+        if workers < 1:
+            raise ValueError("workers must be >= 1")
+        self.workers = workers
+        self.block_rows = block_rows
+        self.block_cols = block_cols
+        self.meter = meter
+        self.trace = trace
+        self.device = device
+
+    def close(self):
+        pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+    def run_wavefront(self, spec: PassSpec) -> PassResult:
+        c1 = np.ascontiguousarray(spec.codes1, dtype=np.uint8)
+        c2 = np.ascontiguousarray(spec.codes2, dtype=np.uint8)
+        if c1.size < 1 or c2.size < 1:
+            raise ValueError("cannot tile an empty matrix")
+        with Session(get_context(self.device), c1, c2, spec.scheme) as S:
+            return S.run([dict(rows=(0, c1.size, 0), cols=(0, c2.size, 0), border=spec.border,
+                               clamp=spec.clamp_zero, track=spec.track, band=spec.band,
+                               prune=spec.prune, want_final=spec.want_final_rows)])[0]
