@@ -199,6 +199,13 @@ int32_t swb_measure_int_peak(swb_ctx* ctx, swb_int_peak* out);
  * (0 = automatic, else 2, 8 or 32 rows of seq1 per lane). */
 int32_t swb_set_option(swb_ctx* ctx, const char* name, int64_t value);
 
+/* Diagnostics: out[0] = cycles warps spent waiting on the strip above,
+ * out[1] = total strip cycles, summed over all passes since "reset_debug". */
+int32_t swb_debug_stats(swb_ctx* ctx, int64_t* out, int32_t n);
+/* Per-strip (start ns, end ns, wait ns) of the most recent pass launch; returns
+ * the number of values available. */
+int32_t swb_debug_times(swb_ctx* ctx, int64_t* out, int32_t n);
+
 /* Device-side timing of the most recent swb_pass launch (ms, CUDA events). */
 double swb_last_kernel_ms(swb_ctx* ctx);
 /* Number of kernels this context launched since creation (for gpu_launches). */

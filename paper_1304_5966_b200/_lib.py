@@ -66,7 +66,8 @@ class IntPeak(ctypes.Structure):
 EXPORTS = (
     "swb_ctx_create", "swb_ctx_destroy", "swb_last_error", "swb_version", "swb_seq_upload",
     "swb_seq_release", "swb_pass", "swb_crossings", "swb_leaves", "swb_measure_int_peak",
-    "swb_last_kernel_ms", "swb_launch_count", "swb_set_option",
+    "swb_last_kernel_ms", "swb_launch_count", "swb_set_option", "swb_debug_stats",
+    "swb_debug_times",
 )
 
 _lib = None
@@ -111,6 +112,10 @@ def load() -> ctypes.CDLL:
         lib.swb_launch_count.restype = c_i64
         lib.swb_set_option.argtypes = [c_p, ctypes.c_char_p, c_i64]
         lib.swb_set_option.restype = c_i32
+        lib.swb_debug_stats.argtypes = [c_p, c_p, c_i32]
+        lib.swb_debug_stats.restype = c_i32
+        lib.swb_debug_times.argtypes = [c_p, c_p, c_i32]
+        lib.swb_debug_times.restype = c_i32
         _lib = lib
         return lib
 

@@ -40,6 +40,9 @@ struct swb_ctx {
   int64_t launches = 0;
   int max_ctas_per_sm = 0;  // 0 = occupancy limit
   int force_R = 0;          // 0 = pick rows-per-lane from the pass height
+  long long dbg_wait_cycles = 0, dbg_strip_cycles = 0;
+  int proto = 2;
+  std::vector<unsigned long long> dbg_times;
   // scratch
   swb_buf jobs, rowbuf, progress, results, finals, misc, host_pinned;
 };

@@ -59,7 +59,9 @@ struct JobDev {
   int32_t* fin_h;        // final row H (DP columns 1..n2) or null
   int32_t* fin_f;
   int4* strip_res;       // per strip (score_m, i, j, has)
-  unsigned long long* counters;  // [0] cells, [1] blocks executed, [2] blocks pruned
+  unsigned long long* strip_times;  // per strip (start ns, end ns, wait ns) diagnostics
+  unsigned long long* counters;  // [0] cells, [1] blocks executed, [2] blocks pruned,
+                                 // [3] cycles spent waiting on the strip above, [4] strip cycles
   int32_t* prune_best;   // running best score (plain) for pruning
 };
 
@@ -70,10 +72,18 @@ struct PassParams {
   int64_t total_items;
   unsigned long long* claim;
   int32_t goe, ge, max_sub;
+  int32_t proto;            // publication protocol variant (diagnostics)
+  int32_t key_mul;          // == 32; opaque to ptxas so the key stays an IMAD
   uint32_t tlo[8], thi[8];  // profile word per column code
 };
 
 __device__ __forceinline__ int vmaxadd(int a, int b, int c) { return __viaddmax_s32(a, b, c); }
+
+__device__ __forceinline__ int imad(int a, int b, int c) {
+  int d;
+  asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
 
 __device__ __forceinline__ uint32_t prmt(uint32_t lo, uint32_t hi, uint32_t sel) {
   uint32_t d;
@@ -89,6 +99,10 @@ __device__ __forceinline__ int ld_acquire(const int32_t* p) {
 
 __device__ __forceinline__ void st_release(int32_t* p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void fence_acq_rel() {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 
 __device__ __forceinline__ int ld_relaxed(const int32_t* p) {
@@ -144,6 +158,14 @@ struct WarpSmem {
   int2 out[32];   // lane-31 outputs of the current 32-step block
 };
 
+// Best-cell tracking without a slow path: every cell's H is folded with its
+// row into a 32-bit key (H - go - ge) * 32 + rank, rank = 31 - r (TRACK_MIN,
+// smaller row wins ties) or r (TRACK_MAX, larger row wins), so one max over
+// the keys of a column yields the best value and the tie-winning row, and a
+// strict (MIN) / non-strict (MAX) comparison against the running key keeps
+// the smallest (MIN) / largest (MAX) column of that row (kernels.py:73-84).
+constexpr int kKeyClamp = -(1 << 25);
+
 template <int R, bool LOCAL, int TRACK, bool FINAL>
 __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, int s,
                                        WarpSmem* sm, const uint32_t* __restrict__ tlo_s,
@@ -186,9 +208,10 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
   }
 
   // Left state at column cb (E holds the value for the column about to run).
-  int H[R], E[R];
+  int H[R], H2[R], E[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
+    H2[r] = 0;
     const int hl = (cb == 0) ? left_h(J.border, lrow0 + r + 1, go, ge) - goe : fillm;
     H[r] = hl;
     E[r] = vmaxadd(SWB_NEG32, -ge, hl);
@@ -202,18 +225,20 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
   } else if (s == 0) {
     diag = top_h(J.border, cb, go, ge) - goe;
   } else if (cb - 1 >= cbp && cb - 1 < cep) {
-    while (ld_acquire(up_progress) < cb) __nanosleep(32);
+    while (ld_relaxed(up_progress) < cb) __nanosleep(20);
+    fence_acq_rel();
     diag = __ldcg(inbuf + (cb - 1)).x;
   } else {
     diag = fillm;
   }
 
-  // Tracking state (kernels.py:73-84): best in the hm frame.
-  int best = (TRACK == kTrackMin) ? -goe : INT32_MIN;
-  int thr = (TRACK == kTrackMin) ? -goe + 1 : INT32_MIN;
-  int bi = -1, bj = -1;
+  int bkey = (TRACK == kTrackMin) ? (-goe) * 32 + 31 : INT32_MIN;
+  // 32 read from the launch parameters so the key multiply-add stays an IMAD
+  // on the FMA pipe instead of a LEA on the (saturated) integer ALU pipe.
+  const int k32 = P.key_mul;
+  int bj = -1;
 
-  int rstar = 0, lstar = -1;
+  int rstar = -1, lstar = -1;
   if (FINAL) {
     const int off = n1 - 1 - R0;
     lstar = off / R;
@@ -222,7 +247,81 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
 
   int out_hm = fillm, out_f = SWB_NEG32;
   long long pruned_blocks = 0, exec_blocks = 0;
+  long long wait_cycles = 0;
+  const long long t_strip0 = clock64();
+  unsigned long long g0, gw = 0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
   const int s_end = ce + 31;
+
+  // One column of this lane's R rows.  GUARD: ramp blocks where some lanes
+  // are outside [cb, ce).
+  auto step = [&](const int k, const int step_no, const bool guard, int (&Hin)[R], int (&Hout)[R]) {
+    const int col = step_no - lane;
+    const int4 rv = sm->ring[col & 63];
+    int up_h = __shfl_up_sync(0xffffffffu, out_hm, 1);
+    int up_f = __shfl_up_sync(0xffffffffu, out_f, 1);
+    if (lane == 0) {
+      up_h = rv.x;
+      up_f = rv.y;
+    }
+    if (!guard || (col >= cb && col < ce)) {
+      const uint32_t tl = (uint32_t)rv.z, th = (uint32_t)rv.w;
+      int d = diag;
+      diag = up_h;
+      int fv = up_f;
+      int hab = up_h;
+      int cm = INT32_MIN, kprev = INT32_MIN;
+      int fh = 0, ff = 0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int sv = (int)prmt(tl, th, sel[r]);
+        const int h2 = LOCAL ? __viaddmax_s32_relu(d, sv, E[r]) : __viaddmax_s32(d, sv, E[r]);
+        fv = vmaxadd(fv, -ge, hab);
+        const int h2m = h2 - goe;
+        const int hm = vmaxadd(fv, -goe, h2m);
+        E[r] = vmaxadd(E[r], -ge, hm);
+        d = Hin[r];
+        Hout[r] = hm;
+        hab = h2m;
+        if (TRACK != kTrackNone) {
+          const int rank = (TRACK == kTrackMin) ? 31 - r : r;
+          // padding rows (i >= n1, last strip only) need no guard: their
+          // values are strictly below a real cell already seen (DESIGN.md
+          // §3.5); a lane whose best decodes to a padding row is dropped.
+          const int key = imad((LOCAL ? hm : (hm > kKeyClamp ? hm : kKeyClamp)), k32, rank);
+          if (r & 1) cm = __vimax3_s32(cm, kprev, key);
+          else if (r == R - 1) cm = cm > key ? cm : key;
+          kprev = key;
+        }
+        if (FINAL && r == rstar) {
+          fh = hm;
+          ff = fv;
+        }
+      }
+      out_hm = Hout[R - 1];
+      out_f = fv;
+      if (TRACK == kTrackMin) {
+        if (cm > bkey) {
+          bkey = cm;
+          bj = col;
+        }
+      } else if (TRACK == kTrackMax) {
+        if (cm >= bkey) {
+          bkey = cm;
+          bj = col;
+        }
+      }
+      if (FINAL && lane == lstar) {
+        J.fin_h[col] = fh + goe;
+        J.fin_f[col] = ff;
+      }
+      if (lane == 31) sm->out[k] = make_int2(out_hm, out_f);
+    } else {
+      // lane outside [cb, ce) in a ramp block: carry the state across
+#pragma unroll
+      for (int r = 0; r < R; ++r) Hout[r] = Hin[r];
+    }
+  };
 
   for (int s0 = cb; s0 < s_end; s0 += 32) {
     // (1) stage lane-0 inputs and profile words for columns [s0, s0 + 32).
@@ -230,7 +329,16 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       const int c = s0 + lane;
       if (s > 0 && s0 < cep && s0 + 32 > cbp) {
         const int need = (s0 + 32 < cep) ? s0 + 32 : cep;
-        while (ld_acquire(up_progress) < need) __nanosleep(64);
+        if (ld_relaxed(up_progress) < need) {
+          const long long tw = clock64();
+          unsigned long long a0, a1;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a0));
+          while (ld_relaxed(up_progress) < need) __nanosleep(20);
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a1));
+          gw += a1 - a0;
+          wait_cycles += clock64() - tw;
+        }
+        fence_acq_rel();
       }
       if (c < ce) {
         int th, tf;
@@ -250,11 +358,12 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       }
       __syncwarp();
     }
+    const bool steady = (s0 - 31 >= cb) && (s0 + 32 <= ce);
 
     // (2) pruning: skip the whole 32-step block when no path through it can
     // reach the running best (phase1.py:24-41, :55-59; strict inequality).
     bool skip = false;
-    if (LOCAL && J.prune && s0 - 31 >= cb && s0 + 32 <= ce) {
+    if (LOCAL && J.prune && steady) {
       int m = out_hm > diag ? out_hm : diag;
 #pragma unroll
       for (int r = 0; r < R; ++r) m = m > H[r] ? m : H[r];
@@ -286,74 +395,19 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     } else {
       ++exec_blocks;
       // (3) 32 steps.
+      // two columns per iteration with ping-pong H registers: the old H of
+      // a row (the next row's diagonal) survives without register moves
+      if (steady) {
 #pragma unroll 1
-      for (int k = 0; k < 32; ++k) {
-        const int step = s0 + k;
-        const int col = step - lane;
-        const int4 rv = sm->ring[col & 63];
-        int up_h = __shfl_up_sync(0xffffffffu, out_hm, 1);
-        int up_f = __shfl_up_sync(0xffffffffu, out_f, 1);
-        if (lane == 0) {
-          up_h = rv.x;
-          up_f = rv.y;
+        for (int k = 0; k < 32; k += 2) {
+          step(k, s0 + k, false, H, H2);
+          step(k + 1, s0 + k + 1, false, H2, H);
         }
-        if (col >= cb && col < ce) {
-          const uint32_t tl = (uint32_t)rv.z, th = (uint32_t)rv.w;
-          int d = diag;
-          diag = up_h;
-          int fv = up_f;
-          int hab = up_h;  // (H or pre-F H) of the row above, minus go+ge
-          int cm = INT32_MIN;
-          int fh = 0, ff = 0;
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            const int sv = (int)prmt(tl, th, sel[r]);
-            const int h2 = LOCAL ? __viaddmax_s32_relu(d, sv, E[r]) : __viaddmax_s32(d, sv, E[r]);
-            fv = vmaxadd(fv, -ge, hab);
-            const int h2m = h2 - goe;
-            const int hm = vmaxadd(fv, -goe, h2m);
-            E[r] = vmaxadd(E[r], -ge, hm);
-            d = H[r];
-            H[r] = hm;
-            hab = h2m;
-            if (TRACK != kTrackNone) {
-              if (r & 1) cm = __vimax3_s32(cm, H[r - 1], hm);
-              else if (r == R - 1) cm = cm > hm ? cm : hm;
-            }
-            if (FINAL && r == rstar) {
-              fh = hm;
-              ff = fv;
-            }
-          }
-          out_hm = H[R - 1];
-          out_f = fv;
-          if (TRACK != kTrackNone) {
-            if (cm >= thr) {
-              // slow path: exact lexicographic update (kernels.py:73-84)
-#pragma unroll
-              for (int r = 0; r < R; ++r) {
-                const int v = H[r];
-                const int i = lrow0 + r;
-                bool upd;
-                if (TRACK == kTrackMin)
-                  upd = (r < nvalid) && v > -goe && (v > best || (v == best && i < bi));
-                else
-                  upd = (r < nvalid) && (v > best || (v == best && i >= bi));
-                if (upd) {
-                  best = v;
-                  bi = i;
-                  bj = col;
-                }
-              }
-              if (TRACK == kTrackMin) thr = best > -goe ? best : -goe + 1;
-              else thr = best;
-            }
-          }
-          if (FINAL && lane == lstar) {
-            J.fin_h[col] = fh + goe;
-            J.fin_f[col] = ff;
-          }
-          if (lane == 31) sm->out[k] = make_int2(out_hm, out_f);
+      } else {
+#pragma unroll 1
+        for (int k = 0; k < 32; k += 2) {
+          step(k, s0 + k, true, H, H2);
+          step(k + 1, s0 + k + 1, true, H2, H);
         }
       }
       __syncwarp();
@@ -363,7 +417,8 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     {
       const int c = s0 - 31 + lane;
       if (c >= cb && c < ce) __stcg(outbuf + c, sm->out[lane]);
-      __threadfence();
+      if (P.proto == 0) __threadfence();
+      else if (P.proto == 1) fence_acq_rel();
       __syncwarp();
       if (lane == 0) {
         int pub = s0 + 1;
@@ -374,15 +429,20 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
 
     // (5) running best for pruning (monotone, never ahead of the truth).
     if (LOCAL && J.prune && TRACK == kTrackMin) {
-      const int bm = __reduce_max_sync(0xffffffffu, best);
+      const int bm = __reduce_max_sync(0xffffffffu, bkey >> 5);
       if (lane == 0 && bm > -goe) atomicMax(J.prune_best, bm + goe);
     }
   }
   if (lane == 0) st_release(my_progress, ce);
 
-  // Strip result: warp reduction with the mode's tie rule (engine.py:247-259).
+  // Strip result: decode the key, then warp reduction with the mode's tie
+  // rule (engine.py:247-259).
   if (TRACK != kTrackNone) {
-    int b = best, ii = bi, jj = bj;
+    int b = bkey >> 5;
+    const int rk = bkey & 31;
+    int ii = (bj >= 0) ? lrow0 + ((TRACK == kTrackMin) ? 31 - rk : rk) : -1;
+    int jj = bj;
+    if (ii >= n1) ii = jj = -1;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const int ob = __shfl_down_sync(0xffffffffu, b, o);
@@ -413,6 +473,13 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     atomicAdd(&J.counters[0], (unsigned long long)(cells > 0 ? cells : 0));
     atomicAdd(&J.counters[1], (unsigned long long)exec_blocks);
     atomicAdd(&J.counters[2], (unsigned long long)pruned_blocks);
+    atomicAdd(&J.counters[3], (unsigned long long)wait_cycles);
+    atomicAdd(&J.counters[4], (unsigned long long)(clock64() - t_strip0));
+    unsigned long long g1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+    J.strip_times[3 * s + 0] = g0;
+    J.strip_times[3 * s + 1] = g1;
+    J.strip_times[3 * s + 2] = gw;
   }
 }
 

@@ -89,19 +89,25 @@ int swb_resolve_seq(swb_ctx* ctx, int32_t id, int64_t off, int64_t len, int32_t 
 
 namespace {
 
-int pick_rows_per_lane(int n1) {
-  if (n1 >= 2048) return 32;
-  if (n1 >= 256) return 8;
-  return 2;
+// Rows-per-lane instantiations.  Local TRACK_MIN passes (phase 1, split) get a
+// dense set so a single large pass can be cut into exactly as many warp-strips
+// as the SM sub-partitions hold; the other modes get a coarse set.
+constexpr int kLocalR[] = {8, 16, 20, 24, 28, 32};
+constexpr int kOtherR[] = {2, 8, 16, 24, 32};
+
+template <int R, bool LOCAL, int TRACK>
+int kernel_occupancy(int* per_sm) {
+  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, pass_kernel<R, LOCAL, TRACK>,
+                                                            128, 0);
 }
 
 template <int R, bool LOCAL, int TRACK>
-int launch_kernel(swb_ctx* ctx, const PassParams& P, long long items, int max_ctas_per_sm) {
+int launch_kernel(swb_ctx* ctx, const PassParams& P, long long items, int ctas_per_sm) {
   auto kern = pass_kernel<R, LOCAL, TRACK>;
   int per_sm = 0;
   SWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, 0));
   if (per_sm < 1) return swb_fail(SWB_ECUDA, "pass kernel does not fit on an SM");
-  if (max_ctas_per_sm > 0 && per_sm > max_ctas_per_sm) per_sm = max_ctas_per_sm;
+  if (ctas_per_sm > 0 && per_sm > ctas_per_sm) per_sm = ctas_per_sm;
   long long cap = (long long)per_sm * ctx->sms;
   long long need = (items + 3) / 4;
   int grid = (int)std::min(cap, std::max(need, 1LL));
@@ -112,15 +118,94 @@ int launch_kernel(swb_ctx* ctx, const PassParams& P, long long items, int max_ct
 }
 
 template <int R>
-int launch_dispatch(swb_ctx* ctx, const PassParams& P, long long items, bool local, int track) {
-  const int cap = ctx->max_ctas_per_sm;
+int dispatch_R(swb_ctx* ctx, const PassParams* P, long long items, bool local, int track,
+               int ctas_per_sm, int* occ_out) {
   if (local) {
-    if (track == kTrackMin) return launch_kernel<R, true, kTrackMin>(ctx, P, items, cap);
-    return swb_fail(SWB_EUNSUPPORTED, "local passes support TRACK_MIN only");
+    if (track != kTrackMin) return swb_fail(SWB_EUNSUPPORTED, "local passes support TRACK_MIN only");
+    if (occ_out) return kernel_occupancy<R, true, kTrackMin>(occ_out);
+    return launch_kernel<R, true, kTrackMin>(ctx, *P, items, ctas_per_sm);
   }
-  if (track == kTrackNone) return launch_kernel<R, false, kTrackNone>(ctx, P, items, cap);
-  if (track == kTrackMin) return launch_kernel<R, false, kTrackMin>(ctx, P, items, cap);
-  return launch_kernel<R, false, kTrackMax>(ctx, P, items, cap);
+  if (track == kTrackNone) {
+    if (occ_out) return kernel_occupancy<R, false, kTrackNone>(occ_out);
+    return launch_kernel<R, false, kTrackNone>(ctx, *P, items, ctas_per_sm);
+  }
+  if (track == kTrackMin) {
+    if (occ_out) return kernel_occupancy<R, false, kTrackMin>(occ_out);
+    return launch_kernel<R, false, kTrackMin>(ctx, *P, items, ctas_per_sm);
+  }
+  if (occ_out) return kernel_occupancy<R, false, kTrackMax>(occ_out);
+  return launch_kernel<R, false, kTrackMax>(ctx, *P, items, ctas_per_sm);
+}
+
+// Launch (P != null) or query occupancy (occ_out != null) for rows-per-lane R.
+int dispatch(swb_ctx* ctx, int R, const PassParams* P, long long items, bool local, int track,
+             int ctas_per_sm, int* occ_out) {
+  if (local) {
+    switch (R) {
+      case 8: return dispatch_R<8>(ctx, P, items, local, track, ctas_per_sm, occ_out);
+      case 16: return dispatch_R<16>(ctx, P, items, local, track, ctas_per_sm, occ_out);
+      case 20: return dispatch_R<20>(ctx, P, items, local, track, ctas_per_sm, occ_out);
+      case 24: return dispatch_R<24>(ctx, P, items, local, track, ctas_per_sm, occ_out);
+      case 28: return dispatch_R<28>(ctx, P, items, local, track, ctas_per_sm, occ_out);
+      case 32: return dispatch_R<32>(ctx, P, items, local, track, ctas_per_sm, occ_out);
+      default: break;
+    }
+  } else {
+    switch (R) {
+      case 2: return dispatch_R<2>(ctx, P, items, local, track, ctas_per_sm, occ_out);
+      case 8: return dispatch_R<8>(ctx, P, items, local, track, ctas_per_sm, occ_out);
+      case 16: return dispatch_R<16>(ctx, P, items, local, track, ctas_per_sm, occ_out);
+      case 24: return dispatch_R<24>(ctx, P, items, local, track, ctas_per_sm, occ_out);
+      case 32: return dispatch_R<32>(ctx, P, items, local, track, ctas_per_sm, occ_out);
+      default: break;
+    }
+  }
+  return swb_fail(SWB_EINVAL, "rows_per_lane %d not instantiated for this pass mode", R);
+}
+
+// Launch-shape model.  A warp-step costs ~5.7 integer-ALU
+// instructions per row at 2 cycles each; a lone warp per SM sub-partition
+// reaches ~60% of that rate, two or more saturate it.  Strips of one pass
+// form a chain, so the pass runs at the pace of the most loaded sub-partition.
+struct Shape {
+  int R = 32;
+  int ctas_per_sm = 0;
+};
+
+Shape choose_shape(swb_ctx* ctx, const std::vector<PassReq*>& jobs, bool local, int track) {
+  const int* cand = local ? kLocalR : kOtherR;
+  const int ncand = local ? (int)(sizeof(kLocalR) / sizeof(int)) : (int)(sizeof(kOtherR) / sizeof(int));
+  const int smsp = ctx->sms * 4;
+  Shape best;
+  double best_t = 1e300;
+  for (int q = 0; q < ncand; ++q) {
+    const int R = cand[q];
+    int occ = 0;
+    if (dispatch(ctx, R, nullptr, 0, local, track, 0, &occ) != cudaSuccess || occ < 1) continue;
+    long long strips = 0, chain = 0;
+    for (const PassReq* r : jobs) {
+      const long long sj = (r->n1 + 32LL * R - 1) / (32LL * R);
+      strips += sj;
+      chain = std::max(chain, (long long)r->n2 + 64LL * sj);
+    }
+    const double alu = 2.0 * (5.7 * R + 10.0);
+    const double lat = 1.7 * alu;
+    const long long w_need = (strips + smsp - 1) / smsp;
+    const int w = (int)std::min<long long>(w_need, occ);
+    const long long rounds = (w_need + occ - 1) / occ;
+    const double step = std::max(w * alu, lat);
+    // total work bound vs chain bound
+    double work = 0.0;
+    for (const PassReq* r : jobs)
+      work += (double)((r->n1 + 32LL * R - 1) / (32LL * R)) * (double)(r->n2 + 64) * alu;
+    const double t = std::max((double)rounds * (double)chain * step, work / smsp);
+    if (t < best_t * 0.999) {
+      best_t = t;
+      best.R = R;
+      best.ctas_per_sm = w;
+    }
+  }
+  return best;
 }
 
 struct Arena {
@@ -148,12 +233,28 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     if (r.n1 < 1 || r.n2 < 1) return swb_fail(SWB_EINVAL, "cannot tile an empty matrix");
     int rc = swb_check_range(sc, r.n1, r.n2);
     if (rc) return rc;
-    r.R = r.force_R ? r.force_R : pick_rows_per_lane(r.n1);
+    // tracked passes fold H and the row rank into one int32 key (H * 32 + rank)
+    if (r.track != kTrackNone &&
+        (long long)std::max(sc.max_sub, 0) * std::min(r.n1, r.n2) + sc.goe >= (1LL << 26) - 64)
+      return swb_fail(SWB_ERANGE, "tracked pass %d x %d exceeds the 26-bit score key range",
+                      r.n1, r.n2);
   }
-  auto key = [&](int q) {
-    const PassReq& r = reqs[q];
-    return (r.local ? 1000 : 0) + r.track * 100 + r.R;
-  };
+  // one launch per (recurrence, tracking) class; rows-per-lane per class
+  auto cls = [&](int q) { return (reqs[q].local ? 10 : 0) + reqs[q].track; };
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cls(a) < cls(b); });
+  std::vector<int> cls_ctas(reqs.size(), 0);
+  for (size_t a = 0; a < order.size();) {
+    size_t b = a;
+    std::vector<PassReq*> js;
+    while (b < order.size() && cls(order[b]) == cls(order[a])) js.push_back(&reqs[order[b++]]);
+    Shape sh = choose_shape(ctx, js, js[0]->local, js[0]->track);
+    for (PassReq* r : js) {
+      r->R = r->force_R ? r->force_R : sh.R;
+      cls_ctas[r - &reqs[0]] = sh.ctas_per_sm;
+    }
+    a = b;
+  }
+  auto key = [&](int q) { return cls(q) * 1000 + reqs[q].R; };
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return key(a) < key(b); });
 
   size_t g0 = 0;
@@ -174,8 +275,8 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
       if (r.want_final && r.fin_h_dev == nullptr) final_cols += r.n2;
     }
     size_t bytes = 256 * 8 + sizeof(JobDev) * nj + sizeof(int32_t) * total_strips +
-                   sizeof(unsigned long long) * 3 * nj + sizeof(int32_t) * nj + 64 +
-                   sizeof(int4) * total_strips + sizeof(int2) * 2 * total_cols +
+                   sizeof(unsigned long long) * 5 * nj + sizeof(int32_t) * nj + 64 +
+                   sizeof(int4) * total_strips + 24 * total_strips + sizeof(int2) * 2 * total_cols +
                    sizeof(int32_t) * 2 * final_cols + 4096 + 256 * 8 * (size_t)nj;
     Arena A;
     A.base = (char*)swb_scratch(ctx->rowbuf, bytes);
@@ -184,14 +285,15 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     // zeroed region
     size_t zero_begin = (A.off + 255) & ~(size_t)255;
     int32_t* d_prog = A.take<int32_t>(total_strips);
-    unsigned long long* d_cnt = A.take<unsigned long long>(3 * nj);
+    unsigned long long* d_cnt = A.take<unsigned long long>(5 * nj);
     int32_t* d_pbest = A.take<int32_t>(nj);
     unsigned long long* d_claim = A.take<unsigned long long>(1);
     size_t zero_end = A.off;
     int4* d_res = A.take<int4>(total_strips);
+    unsigned long long* d_times = A.take<unsigned long long>(3 * total_strips);
     // host staging (pinned)
     size_t hbytes = sizeof(JobDev) * nj + sizeof(int4) * total_strips +
-                    sizeof(unsigned long long) * 3 * nj + 1024;
+                    sizeof(unsigned long long) * 5 * nj + 1024;
     char* hbase = (char*)swb_scratch_host(ctx->host_pinned, hbytes);
     if (!hbase) return swb_fail(SWB_ECUDA, "pinned host allocation failed");
     JobDev* h_jobs = reinterpret_cast<JobDev*>(hbase);
@@ -227,7 +329,8 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
       J.buf[1] = A.take<int2>(r.n2);
       J.progress = d_prog + strip_off;
       J.strip_res = d_res + strip_off;
-      J.counters = d_cnt + 3 * t;
+      J.strip_times = d_times + 3 * strip_off;
+      J.counters = d_cnt + 5 * t;
       J.prune_best = d_pbest + t;
       if (r.want_final) {
         if (r.fin_h_dev) {
@@ -268,21 +371,24 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     P.goe = sc.goe;
     P.ge = sc.ge;
     P.max_sub = sc.max_sub;
+    P.proto = ctx->proto;
+    P.key_mul = 32;
     memcpy(P.tlo, sc.tlo, sizeof(P.tlo));
     memcpy(P.thi, sc.thi, sizeof(P.thi));
 
     SWB_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
     int rc;
-    if (R == 32) rc = launch_dispatch<32>(ctx, P, item, head.local, head.track);
-    else if (R == 8) rc = launch_dispatch<8>(ctx, P, item, head.local, head.track);
-    else rc = launch_dispatch<2>(ctx, P, item, head.local, head.track);
+    int ctas = ctx->max_ctas_per_sm ? ctx->max_ctas_per_sm : cls_ctas[order[g0]];
+    rc = dispatch(ctx, R, &P, item, head.local, head.track, ctas, nullptr);
     if (rc) return rc;
     SWB_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
     SWB_CUDA(cudaMemcpyAsync(h_res, d_res, sizeof(int4) * total_strips, cudaMemcpyDeviceToHost,
                              ctx->stream));
-    SWB_CUDA(cudaMemcpyAsync(h_cnt, d_cnt, sizeof(unsigned long long) * 3 * nj,
+    SWB_CUDA(cudaMemcpyAsync(h_cnt, d_cnt, sizeof(unsigned long long) * 5 * nj,
                              cudaMemcpyDeviceToHost, ctx->stream));
     SWB_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->dbg_times.resize(3 * total_strips);
+    SWB_CUDA(cudaMemcpy(ctx->dbg_times.data(), d_times, 24 * total_strips, cudaMemcpyDeviceToHost));
     float ms = 0.f;
     SWB_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
     ctx->last_kernel_ms = ms;
@@ -324,9 +430,11 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
       r.best_score = bs;
       r.best_i = bi;
       r.best_j = bj;
-      r.cells = (long long)h_cnt[3 * t + 0];
-      r.blocks_exec = (long long)h_cnt[3 * t + 1];
-      r.blocks_pruned = (long long)h_cnt[3 * t + 2];
+      r.cells = (long long)h_cnt[5 * t + 0];
+      r.blocks_exec = (long long)h_cnt[5 * t + 1];
+      r.blocks_pruned = (long long)h_cnt[5 * t + 2];
+      ctx->dbg_wait_cycles += (long long)h_cnt[5 * t + 3];
+      ctx->dbg_strip_cycles += (long long)h_cnt[5 * t + 4];
       r.blocks_total = (long long)r.nstrips * ((r.n2 + 31) / 32);
     }
     g0 = g1;
@@ -365,9 +473,17 @@ extern "C" int32_t swb_set_option(swb_ctx* ctx, const char* name, int64_t value)
     ctx->max_ctas_per_sm = (int)value;
     return SWB_OK;
   }
+  if (!strcmp(name, "proto")) {
+    ctx->proto = (int)value;
+    return SWB_OK;
+  }
+  if (!strcmp(name, "reset_debug")) {
+    ctx->dbg_wait_cycles = ctx->dbg_strip_cycles = 0;
+    return SWB_OK;
+  }
   if (!strcmp(name, "rows_per_lane")) {
-    if (value != 0 && value != 2 && value != 8 && value != 32)
-      return swb_fail(SWB_EINVAL, "rows_per_lane must be 0 (auto), 2, 8 or 32");
+    if (value < 0 || value > 32)
+      return swb_fail(SWB_EINVAL, "rows_per_lane must be 0 (auto) or an instantiated value <= 32");
     ctx->force_R = (int)value;
     return SWB_OK;
   }
@@ -441,4 +557,18 @@ extern "C" int32_t swb_pass(swb_ctx* ctx, const swb_scheme* scheme, const swb_pa
     }
   }
   SWB_API_END();
+}
+
+extern "C" int32_t swb_debug_times(swb_ctx* ctx, int64_t* out, int32_t n) {
+  if (!ctx || !out) return swb_fail(SWB_EINVAL, "bad arguments");
+  int32_t m = (int32_t)ctx->dbg_times.size();
+  for (int32_t q = 0; q < n && q < m; ++q) out[q] = (int64_t)ctx->dbg_times[q];
+  return m;
+}
+
+extern "C" int32_t swb_debug_stats(swb_ctx* ctx, int64_t* out, int32_t n) {
+  if (!ctx || !out) return swb_fail(SWB_EINVAL, "bad arguments");
+  const int64_t v[2] = {ctx->dbg_wait_cycles, ctx->dbg_strip_cycles};
+  for (int q = 0; q < n && q < 2; ++q) out[q] = v[q];
+  return SWB_OK;
 }

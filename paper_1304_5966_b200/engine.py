@@ -127,6 +127,17 @@ class DeviceContext:
     def set_option(self, name: str, value: int) -> None:
         _lib.check(self.lib.swb_set_option(self.ptr, name.encode(), int(value)), "swb_set_option")
 
+    def debug_stats(self) -> dict:
+        out = (ctypes.c_int64 * 2)()
+        _lib.check(self.lib.swb_debug_stats(self.ptr, out, 2), "swb_debug_stats")
+        return {"wait_cycles": int(out[0]), "strip_cycles": int(out[1])}
+
+    def debug_times(self) -> np.ndarray:
+        n = int(self.lib.swb_debug_times(self.ptr, None, 0)) if False else 1 << 20
+        out = np.zeros(n, dtype=np.int64)
+        m = self.lib.swb_debug_times(self.ptr, out.ctypes.data, n)
+        return out[:max(0, min(m, n))].reshape(-1, 3)
+
     @property
     def launch_count(self) -> int:
         return int(self.lib.swb_launch_count(self.ptr))
