@@ -206,6 +206,14 @@ int32_t swb_debug_stats(swb_ctx* ctx, int64_t* out, int32_t n);
  * the number of values available. */
 int32_t swb_debug_times(swb_ctx* ctx, int64_t* out, int32_t n);
 
+/* CUDA events on the context's stream around a caller-defined region
+ * (bench timing of K steps on the launching stream). */
+int32_t swb_timer_start(swb_ctx* ctx);
+int32_t swb_timer_stop(swb_ctx* ctx, double* ms);
+/* Overwrite `bytes` (0: 512 MiB, > the 126 MB L2) of scratch on the stream to
+ * evict earlier working sets from L2 between timed steps. */
+int32_t swb_flush_l2(swb_ctx* ctx, int64_t bytes);
+
 /* Device-side timing of the most recent swb_pass launch (ms, CUDA events). */
 double swb_last_kernel_ms(swb_ctx* ctx);
 /* Number of kernels this context launched since creation (for gpu_launches). */

@@ -67,7 +67,7 @@ EXPORTS = (
     "swb_ctx_create", "swb_ctx_destroy", "swb_last_error", "swb_version", "swb_seq_upload",
     "swb_seq_release", "swb_pass", "swb_crossings", "swb_leaves", "swb_measure_int_peak",
     "swb_last_kernel_ms", "swb_launch_count", "swb_set_option", "swb_debug_stats",
-    "swb_debug_times",
+    "swb_debug_times", "swb_timer_start", "swb_timer_stop", "swb_flush_l2",
 )
 
 _lib = None
@@ -116,6 +116,12 @@ def load() -> ctypes.CDLL:
         lib.swb_debug_stats.restype = c_i32
         lib.swb_debug_times.argtypes = [c_p, c_p, c_i32]
         lib.swb_debug_times.restype = c_i32
+        lib.swb_timer_start.argtypes = [c_p]
+        lib.swb_timer_start.restype = c_i32
+        lib.swb_timer_stop.argtypes = [c_p, ctypes.POINTER(ctypes.c_double)]
+        lib.swb_timer_stop.restype = c_i32
+        lib.swb_flush_l2.argtypes = [c_p, c_i64]
+        lib.swb_flush_l2.restype = c_i32
         _lib = lib
         return lib
 

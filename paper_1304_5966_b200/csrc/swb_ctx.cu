@@ -110,7 +110,11 @@ void swb_ctx_destroy(swb_ctx* ctx) {
     if (s.rev) cudaFree(s.rev);
   }
   swb_buf* bufs[] = {&ctx->jobs, &ctx->rowbuf, &ctx->progress, &ctx->results, &ctx->finals,
-                     &ctx->misc};
+                     &ctx->misc, &ctx->flush};
+  if (ctx->tev0) {
+    cudaEventDestroy(ctx->tev0);
+    cudaEventDestroy(ctx->tev1);
+  }
   for (auto* b : bufs)
     if (b->p) cudaFree(b->p);
   if (ctx->host_pinned.p) cudaFreeHost(ctx->host_pinned.p);
@@ -168,6 +172,37 @@ int32_t swb_seq_release(swb_ctx* ctx, int32_t seq_id) {
 }
 
 double swb_last_kernel_ms(swb_ctx* ctx) { return ctx ? ctx->last_kernel_ms : 0.0; }
+
+int32_t swb_timer_start(swb_ctx* ctx) {
+  SWB_API_BEGIN(ctx);
+  if (!ctx->tev0) {
+    SWB_CUDA(cudaEventCreate(&ctx->tev0));
+    SWB_CUDA(cudaEventCreate(&ctx->tev1));
+  }
+  SWB_CUDA(cudaEventRecord(ctx->tev0, ctx->stream));
+  SWB_API_END();
+}
+
+int32_t swb_timer_stop(swb_ctx* ctx, double* ms) {
+  SWB_API_BEGIN(ctx);
+  if (!ctx->tev0 || !ms) return swb_fail(SWB_EINVAL, "timer not started");
+  SWB_CUDA(cudaEventRecord(ctx->tev1, ctx->stream));
+  SWB_CUDA(cudaEventSynchronize(ctx->tev1));
+  float f = 0.f;
+  SWB_CUDA(cudaEventElapsedTime(&f, ctx->tev0, ctx->tev1));
+  *ms = f;
+  SWB_API_END();
+}
+
+int32_t swb_flush_l2(swb_ctx* ctx, int64_t bytes) {
+  SWB_API_BEGIN(ctx);
+  if (bytes <= 0) bytes = 512LL << 20;
+  void* p = swb_scratch(ctx->flush, (size_t)bytes);
+  if (!p) return swb_fail(SWB_ECUDA, "cannot allocate the L2 flush buffer");
+  SWB_CUDA(cudaMemsetAsync(p, (int)(ctx->launches & 0xff), (size_t)bytes, ctx->stream));
+  SWB_CUDA(cudaStreamSynchronize(ctx->stream));
+  SWB_API_END();
+}
 
 int64_t swb_launch_count(swb_ctx* ctx) { return ctx ? ctx->launches : 0; }
 

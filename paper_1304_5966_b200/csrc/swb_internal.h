@@ -44,7 +44,8 @@ struct swb_ctx {
   int proto = 2;
   std::vector<unsigned long long> dbg_times;
   // scratch
-  swb_buf jobs, rowbuf, progress, results, finals, misc, host_pinned;
+  swb_buf jobs, rowbuf, progress, results, finals, misc, host_pinned, flush;
+  cudaEvent_t tev0 = nullptr, tev1 = nullptr;
 };
 
 void swb_set_error(const char* fmt, ...);

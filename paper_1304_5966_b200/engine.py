@@ -127,6 +127,17 @@ class DeviceContext:
     def set_option(self, name: str, value: int) -> None:
         _lib.check(self.lib.swb_set_option(self.ptr, name.encode(), int(value)), "swb_set_option")
 
+    def timer_start(self) -> None:
+        _lib.check(self.lib.swb_timer_start(self.ptr), "swb_timer_start")
+
+    def timer_stop(self) -> float:
+        ms = ctypes.c_double()
+        _lib.check(self.lib.swb_timer_stop(self.ptr, ctypes.byref(ms)), "swb_timer_stop")
+        return float(ms.value)
+
+    def flush_l2(self, nbytes: int = 0) -> None:
+        _lib.check(self.lib.swb_flush_l2(self.ptr, int(nbytes)), "swb_flush_l2")
+
     def debug_stats(self) -> dict:
         out = (ctypes.c_int64 * 2)()
         _lib.check(self.lib.swb_debug_stats(self.ptr, out, 2), "swb_debug_stats")
