@@ -42,6 +42,7 @@ struct swb_ctx {
   int force_R = 0;          // 0 = pick rows-per-lane from the pass height
   long long dbg_wait_cycles = 0, dbg_strip_cycles = 0;
   int proto = 2;
+  int claim_mode = 0;
   std::vector<unsigned long long> dbg_times;
   // scratch
   swb_buf jobs, rowbuf, progress, results, finals, misc, host_pinned, flush;

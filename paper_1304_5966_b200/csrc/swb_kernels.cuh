@@ -74,6 +74,8 @@ struct PassParams {
   int32_t goe, ge, max_sub;
   int32_t proto;            // publication protocol variant (diagnostics)
   int32_t key_mul;          // == 32; opaque to ptxas so the key stays an IMAD
+  int32_t group;            // > 0: CTA-level claiming of `group` strips (see pass_kernel)
+  int32_t mirror;           // CTA mode, single round, 2 warps/sub-partition: mirror pairs
   uint32_t tlo[8], thi[8];  // profile word per column code
 };
 
@@ -484,9 +486,37 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
 }
 
 template <int R, bool LOCAL, int TRACK>
-__global__ void __launch_bounds__(128) pass_kernel(const PassParams P) {
-  __shared__ WarpSmem wsm[4];
+__device__ __forceinline__ void run_item(const PassParams& P, long long item, WarpSmem* sm,
+                                         const uint32_t* tlo_s, const uint32_t* thi_s) {
+  // locate the pass owning this item (jobs sorted by item_base)
+  int lo = 0, hi = P.njobs - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (P.jobs[mid].item_base <= item) lo = mid;
+    else hi = mid - 1;
+  }
+  const JobDev& J = P.jobs[lo];
+  const int s = (int)(item - J.item_base);
+  if (J.want_final && s == J.nstrips - 1)
+    run_strip<R, LOCAL, TRACK, true>(P, J, s, sm, tlo_s, thi_s);
+  else
+    run_strip<R, LOCAL, TRACK, false>(P, J, s, sm, tlo_s, thi_s);
+}
+
+// Persistent launch.  Two claiming modes:
+//  * P.group == 0: every warp claims one strip at a time (many small passes,
+//    e.g. a Myers-Miller level).
+//  * P.group  > 0: one CTA per SM with 4*w warps (w per SM sub-partition)
+//    claims 4*w consecutive strips at once; warp i runs on sub-partition i % 4
+//    and takes strip base + (i % 4) * w + i / 4, so the w warps sharing a
+//    sub-partition hold ADJACENT strips of the chain: when one waits for its
+//    producer the other (its producer or consumer) gets the issue slots, and
+//    every sub-partition carries the same load.
+template <int R, bool LOCAL, int TRACK>
+__global__ void __launch_bounds__(256) pass_kernel(const PassParams P) {
+  __shared__ WarpSmem wsm[8];
   __shared__ uint32_t tlo_s[8], thi_s[8];
+  __shared__ long long base_s;
   if (threadIdx.x < 8) {
     tlo_s[threadIdx.x] = P.tlo[threadIdx.x];
     thi_s[threadIdx.x] = P.thi[threadIdx.x];
@@ -495,24 +525,34 @@ __global__ void __launch_bounds__(128) pass_kernel(const PassParams P) {
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   WarpSmem* sm = &wsm[warp];
+  if (P.group > 0) {
+    const int w = (int)(blockDim.x >> 7);
+    for (;;) {
+      if (threadIdx.x == 0) base_s = (long long)atomicAdd(P.claim, (unsigned long long)P.group);
+      __syncthreads();
+      const long long base = base_s;
+      __syncthreads();
+      if (base >= P.total_items) break;
+      long long item = base + (warp & 3) * w + (warp >> 2);
+      if (P.mirror) {
+        // single round, two warps per sub-partition: sub-partition p holds
+        // strips p and total-1-p.  The top strips (never pruned, on the
+        // critical path) share issue slots with bottom strips, which are idle
+        // during the pipeline ramp and mostly pruned.
+        const long long p = base / 2 + (warp & 3);
+        const long long q = P.total_items - 1 - p;
+        item = (warp >> 2) == 0 ? (p <= q ? p : P.total_items) : (p < q ? q : P.total_items);
+      }
+      if (item < P.total_items) run_item<R, LOCAL, TRACK>(P, item, sm, tlo_s, thi_s);
+    }
+    return;
+  }
   for (;;) {
     long long item = 0;
     if (lane == 0) item = (long long)atomicAdd(P.claim, 1ULL);
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item >= P.total_items) break;
-    // locate the pass owning this item (jobs sorted by item_base)
-    int lo = 0, hi = P.njobs - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (P.jobs[mid].item_base <= item) lo = mid;
-      else hi = mid - 1;
-    }
-    const JobDev& J = P.jobs[lo];
-    const int s = (int)(item - J.item_base);
-    if (J.want_final && s == J.nstrips - 1)
-      run_strip<R, LOCAL, TRACK, true>(P, J, s, sm, tlo_s, thi_s);
-    else
-      run_strip<R, LOCAL, TRACK, false>(P, J, s, sm, tlo_s, thi_s);
+    run_item<R, LOCAL, TRACK>(P, item, sm, tlo_s, thi_s);
   }
 }
 

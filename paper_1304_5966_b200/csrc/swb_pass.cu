@@ -102,12 +102,33 @@ int kernel_occupancy(int* per_sm) {
 }
 
 template <int R, bool LOCAL, int TRACK>
-int launch_kernel(swb_ctx* ctx, const PassParams& P, long long items, int ctas_per_sm) {
+int launch_kernel(swb_ctx* ctx, const PassParams& Pin, long long items, int ctas_per_sm) {
   auto kern = pass_kernel<R, LOCAL, TRACK>;
+  PassParams P = Pin;
   int per_sm = 0;
   SWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, 0));
   if (per_sm < 1) return swb_fail(SWB_ECUDA, "pass kernel does not fit on an SM");
   if (ctas_per_sm > 0 && per_sm > ctas_per_sm) per_sm = ctas_per_sm;
+  if (ctx->claim_mode != 2 && (ctx->claim_mode == 1 || P.njobs <= 4) && per_sm <= 2 &&
+      items > (long long)ctx->sms * 4) {
+    // one CTA per SM, per_sm warps per sub-partition, adjacent strips paired
+    const int threads = 128 * per_sm;
+    int fit = 0;
+    SWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, kern, threads, 0));
+    if (fit >= 1) {
+      P.group = 4 * per_sm;
+      P.mirror = (per_sm == 2 && items <= 8LL * ctx->sms && ctx->proto != 8) ? 1 : 0;
+      // dynamic shared memory pins the layout to exactly one CTA per SM
+      const int pin = 120 * 1024;
+      SWB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pin));
+      kern<<<ctx->sms, threads, pin, ctx->stream>>>(P);
+      ctx->launches++;
+      SWB_CUDA(cudaGetLastError());
+      return SWB_OK;
+    }
+  }
+  P.group = 0;
+  P.mirror = 0;
   long long cap = (long long)per_sm * ctx->sms;
   long long need = (items + 3) / 4;
   int grid = (int)std::min(cap, std::max(need, 1LL));
@@ -471,6 +492,10 @@ extern "C" int32_t swb_set_option(swb_ctx* ctx, const char* name, int64_t value)
   if (!ctx || !name) return swb_fail(SWB_EINVAL, "bad arguments");
   if (!strcmp(name, "max_ctas_per_sm")) {
     ctx->max_ctas_per_sm = (int)value;
+    return SWB_OK;
+  }
+  if (!strcmp(name, "claim_mode")) {
+    ctx->claim_mode = (int)value;  // 0 auto, 1 force CTA claiming, 2 force warp claiming
     return SWB_OK;
   }
   if (!strcmp(name, "proto")) {

@@ -23,13 +23,17 @@ for spec in sys.argv[1:]:
     ctx.set_option("max_ctas_per_sm", ctas)
     proto = 2
     rpl = 0
+    claim = 0
     for o in opt:
+        if o.startswith("claim="):
+            claim = int(o[6:])
         if o.startswith("R="):
             rpl = int(o[2:])
         if o.startswith("proto="):
             proto = int(o[6:])
     ctx.set_option("proto", proto)
     ctx.set_option("rows_per_lane", rpl)
+    ctx.set_option("claim_mode", claim)
     rng = np.random.default_rng(7)
     a = random_codes(rng, n1)
     if kind == "hom":
