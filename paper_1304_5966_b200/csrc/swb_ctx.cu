@@ -1,6 +1,7 @@
 // Context, error reporting, sequence upload and scratch management for libswb.so.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "swb_internal.h"
@@ -91,6 +92,7 @@ swb_ctx* swb_ctx_create(int32_t device) {
   }
   swb_ctx* ctx = new swb_ctx();
   ctx->device = device;
+  ctx->trace = getenv("SWB_TRACE") != nullptr;
   ctx->sms = prop.multiProcessorCount;
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess) {

@@ -43,6 +43,7 @@ struct swb_ctx {
   long long dbg_wait_cycles = 0, dbg_strip_cycles = 0;
   int proto = 2;
   int claim_mode = 0;
+  bool trace = false;
   std::vector<unsigned long long> dbg_times;
   // scratch
   swb_buf jobs, rowbuf, progress, results, finals, misc, host_pinned, flush;

@@ -414,6 +414,20 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     SWB_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
     ctx->last_kernel_ms = ms;
     if (kernel_ms_total) *kernel_ms_total += ms;
+    if (ctx->trace) {
+      long long cells = 0, maxn1 = 0, maxn2 = 0;
+      for (int t = 0; t < nj; ++t) {
+        const PassReq& r = reqs[order[g0 + t]];
+        maxn1 = std::max<long long>(maxn1, r.n1);
+        maxn2 = std::max<long long>(maxn2, r.n2);
+      }
+      for (int t = 0; t < nj; ++t) cells += (long long)h_cnt[5 * t + 0];
+      fprintf(stderr,
+              "[swb] launch local=%d track=%d R=%d jobs=%d strips=%lld max_n1=%lld max_n2=%lld "
+              "cells=%lld ms=%.3f gcups=%.1f\n",
+              (int)head.local, head.track, R, nj, total_strips, maxn1, maxn2, cells, ms,
+              cells / (ms * 1e6));
+    }
 
     for (int t = 0; t < nj; ++t) {
       PassReq& r = reqs[order[g0 + t]];

@@ -109,7 +109,8 @@ def _split_level(S: Session, level: np.ndarray, band: bool) -> np.ndarray:
     return kids
 
 
-def collect_leaves(S: Session, root: np.ndarray, leaf_limit: int, band: bool) -> np.ndarray:
+def collect_leaves(S: Session, root: np.ndarray, leaf_limit: int, band: bool,
+                   stats: dict | None = None) -> np.ndarray:
     """Breadth-first Myers-Miller recursion; returns the leaves in path order."""
     frontier = root
     done = np.zeros(frontier.shape[0], dtype=bool)
@@ -117,6 +118,9 @@ def collect_leaves(S: Session, root: np.ndarray, leaf_limit: int, band: bool) ->
     while True:
         leaf = done | _is_leaf(frontier, leaf_limit)
         if leaf.all():
+            if stats is not None:
+                stats["mm_levels"] = stats.get("mm_levels", 0) + levels
+                stats["mm_leaves"] = stats.get("mm_leaves", 0) + int(frontier.shape[0])
             return frontier
         inner = np.flatnonzero(~leaf)
         kids = _split_level(S, frontier[inner], band)
@@ -180,18 +184,26 @@ def solve_leaves(S: Session, leaves: np.ndarray, band: bool) -> np.ndarray:
 
 
 def solve_rect(S: Session, sub: Subproblem, leaf_limit: int = DEFAULT_LEAF_LIMIT,
-               band: bool = True) -> np.ndarray:
+               band: bool = True, stats: dict | None = None) -> np.ndarray:
     """Full op sequence of one known-score rectangle (phase3.py:250-286)."""
-    leaves = collect_leaves(S, _as_array([sub]), leaf_limit, band)
-    return solve_leaves(S, leaves, band)
+    import time
+    t0 = time.perf_counter()
+    leaves = collect_leaves(S, _as_array([sub]), leaf_limit, band, stats)
+    t1 = time.perf_counter()
+    ops = solve_leaves(S, leaves, band)
+    if stats is not None:
+        stats["t_crossings"] = stats.get("t_crossings", 0.0) + (t1 - t0)
+        stats["t_leaves"] = stats.get("t_leaves", 0.0) + (time.perf_counter() - t1)
+    return ops
 
 
 def reconstruct(S: Session, summary: AlignmentSummary, leaf_limit: int = DEFAULT_LEAF_LIMIT,
-                band: bool = True) -> AlignmentPath:
+                band: bool = True, stats: dict | None = None) -> AlignmentPath:
     """Full path for a summary from phases 1 and 2 (phase3.py:289-312)."""
     if summary.score == 0:
         return AlignmentPath.empty()
-    ops = solve_rect(S, Subproblem(summary.start, summary.end, summary.score), leaf_limit, band)
+    ops = solve_rect(S, Subproblem(summary.start, summary.end, summary.score), leaf_limit, band,
+                     stats)
     path = AlignmentPath(summary.start, ops)
     achieved = score_of_path(path, _Seq(S.codes1), _Seq(S.codes2), S.scheme)
     if achieved != summary.score:

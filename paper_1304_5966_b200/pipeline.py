@@ -6,6 +6,7 @@ every DP pass, crossing and leaf runs on the B200 through libswb.so.
 from __future__ import annotations
 
 import logging
+import time
 from dataclasses import dataclass
 
 from . import phase1, phase2, phase3
@@ -65,7 +66,9 @@ def align(seq1: Sequence, seq2: Sequence, scheme: ScoringScheme,
             if report is not None:
                 report.update(device_kernel_ms=S.kernel_ms, device_cells=S.cells)
             return out
+        t0 = time.perf_counter()
         scored, p1 = phase1.best_local(S, cfg.prune)
+        t1 = time.perf_counter()
         _report_phase1(report, scored, p1, S)
         if scored.score == 0:
             return AlignmentSummary.empty(), AlignmentPath.empty()
@@ -74,10 +77,13 @@ def align(seq1: Sequence, seq2: Sequence, scheme: ScoringScheme,
             e = scored.end
             band = phase2.compute_band(scored.score, min(e.i, e.j), max(e.i, e.j), scheme)
         start = phase2.locate_start(S, scored.end, scored.score, band)
+        t2 = time.perf_counter()
         summary = AlignmentSummary(scored.score, start, scored.end)
-        path = phase3.reconstruct(S, summary, cfg.leaf_limit, cfg.band)
+        path = phase3.reconstruct(S, summary, cfg.leaf_limit, cfg.band, stats=report)
+        t3 = time.perf_counter()
         if report is not None:
-            report.update(device_kernel_ms=S.kernel_ms, device_cells=S.cells)
+            report.update(device_kernel_ms=S.kernel_ms, device_cells=S.cells,
+                          phase_seconds=(t1 - t0, t2 - t1, t3 - t2))
         return summary, path
 
 
