@@ -39,6 +39,7 @@ class _Pass(ctypes.Structure):
         ("block_rows", ctypes.c_int64), ("block_cols", ctypes.c_int64),
         ("threads", ctypes.c_int32),
         ("top_h", ctypes.c_void_p), ("top_f", ctypes.c_void_p),
+        ("row_offset", ctypes.c_int64),
     ]
 
 
@@ -123,10 +124,13 @@ class PassOut:
 
 
 def run_wavefront(c1, c2, scheme: OracleScheme, border: str, clamp0: bool, track: int,
-                  band=None, prune=False, fill_h=None, block=(512, 512), threads=None) -> PassOut:
+                  band=None, prune=False, fill_h=None, block=(512, 512), threads=None,
+                  top=None, row_offset=0) -> PassOut:
     """engine.WavefrontEngine.run_wavefront (engine.py:188-282) with the border
     family of engine.py:340-401 and, when prune, the phase-1 hook
-    (phase1.py:55-59)."""
+    (phase1.py:55-59).  `top` = (top_h, top_f) replaces the family's top
+    border and `row_offset` shifts the left border (a row slab of a larger
+    pass whose rows above produced `top`)."""
     c1 = np.ascontiguousarray(c1, dtype=np.uint8)
     c2 = np.ascontiguousarray(c2, dtype=np.uint8)
     sub = np.ascontiguousarray(scheme.sub, dtype=np.int64)
@@ -134,7 +138,12 @@ def run_wavefront(c1, c2, scheme: OracleScheme, border: str, clamp0: bool, track
     top_h = np.empty(n2 + 1, dtype=np.int64)
     top_f = np.empty(n2 + 1, dtype=np.int64)
     lib = _lib()
-    lib.orc_top_border(BORDER[border], n2, scheme.gap_open, scheme.gap_extend, _c(top_h), _c(top_f))
+    if top is None:
+        lib.orc_top_border(BORDER[border], n2, scheme.gap_open, scheme.gap_extend, _c(top_h),
+                           _c(top_f))
+    else:
+        top_h[:] = top[0]
+        top_f[:] = top[1]
     p = _Pass()
     p.c1, p.n1, p.c2, p.n2 = _c(c1), c1.size, _c(c2), n2
     p.sub, p.k, p.border = _c(sub), sub.shape[0], BORDER[border]
@@ -147,6 +156,7 @@ def run_wavefront(c1, c2, scheme: OracleScheme, border: str, clamp0: bool, track
     p.block_rows, p.block_cols = block
     p.threads = int(threads or max_threads())
     p.top_h, p.top_f = _c(top_h), _c(top_f)
+    p.row_offset = int(row_offset)
     r = _Result()
     rc = lib.orc_run_wavefront(ctypes.byref(p), ctypes.byref(r))
     if rc != 0:

@@ -150,6 +150,7 @@ typedef struct {
   int32_t threads;
   int64_t* top_h; /* n2+1, in/out (becomes the final row) */
   int64_t* top_f;
+  int64_t row_offset; /* DP row of this pass's row 0 within a larger pass (row slabs) */
 } orc_pass;
 
 typedef struct {
@@ -178,10 +179,10 @@ int orc_run_wavefront(const orc_pass* P, orc_result* out) {
     const int64_t r0 = bi * br;
     const int64_t r1 = r0 + br < rows ? r0 + br : rows;
     int64_t h, e, f;
-    border_left(P->border, r0, P->go, P->ge, &h, &e, &f);
+    border_left(P->border, P->row_offset + r0, P->go, P->ge, &h, &e, &f);
     corner[bi] = h;
     for (int64_t r = r0; r < r1; ++r) {
-      border_left(P->border, r + 1, P->go, P->ge, &h, &e, &f);
+      border_left(P->border, P->row_offset + r + 1, P->go, P->ge, &h, &e, &f);
       col_h[r] = h;
       col_e[r] = e;
     }
@@ -254,7 +255,7 @@ int orc_run_wavefront(const orc_pass* P, orc_result* out) {
   }
   {
     int64_t h, e, f;
-    border_left(P->border, rows, P->go, P->ge, &h, &e, &f);
+    border_left(P->border, P->row_offset + rows, P->go, P->ge, &h, &e, &f);
     row_h[0] = h;
     row_f[0] = f;
   }
