@@ -248,6 +248,8 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
   }
 
   int out_hm = fillm, out_f = SWB_NEG32;
+  int known_prog = 0, prune_seen = 0;
+  int code_next = (cb + lane < ce) ? (int)J.cols[(long long)(cb + lane) * J.cstep] : 0;
   long long pruned_blocks = 0, exec_blocks = 0;
   long long wait_cycles = 0;
   const long long t_strip0 = clock64();
@@ -327,20 +329,31 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
 
   for (int s0 = cb; s0 < s_end; s0 += 32) {
     // (1) stage lane-0 inputs and profile words for columns [s0, s0 + 32).
+    // The column codes were prefetched one block ahead; the producer's
+    // progress is polled only when the last observed value does not cover
+    // this block, and acquired with one ld.acquire.
     {
       const int c = s0 + lane;
+      const int code = code_next;
+      const int pb_now = (LOCAL && J.prune) ? ld_relaxed(J.prune_best) : 0;
+      {
+        const int cn = c + 32;
+        code_next = (cn < ce) ? (int)J.cols[(long long)cn * J.cstep] : 0;
+      }
       if (s > 0 && s0 < cep && s0 + 32 > cbp) {
         const int need = (s0 + 32 < cep) ? s0 + 32 : cep;
-        if (ld_relaxed(up_progress) < need) {
-          const long long tw = clock64();
-          unsigned long long a0, a1;
-          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a0));
-          while (ld_relaxed(up_progress) < need) __nanosleep(20);
-          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a1));
-          gw += a1 - a0;
-          wait_cycles += clock64() - tw;
+        if (known_prog < need) {
+          if (ld_relaxed(up_progress) < need) {
+            const long long tw = clock64();
+            unsigned long long a0, a1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a0));
+            while (ld_relaxed(up_progress) < need) __nanosleep(20);
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a1));
+            gw += a1 - a0;
+            wait_cycles += clock64() - tw;
+          }
+          known_prog = ld_acquire(up_progress);
         }
-        fence_acq_rel();
       }
       if (c < ce) {
         int th, tf;
@@ -355,9 +368,9 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
           th = fillm;
           tf = SWB_NEG32;
         }
-        const int code = J.cols[(long long)c * J.cstep];
         sm->ring[c & 63] = make_int4(th, tf, (int)tlo_s[code], (int)thi_s[code]);
       }
+      prune_seen = pb_now;
       __syncwarp();
     }
     const bool steady = (s0 - 31 >= cb) && (s0 + 32 <= ce);
@@ -377,8 +390,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       const int rem_c = n2 - (s0 - 31);
       const long long bound =
           (long long)inmax + (long long)P.max_sub * (long long)(rem_r < rem_c ? rem_r : rem_c);
-      const int pb = ld_relaxed(J.prune_best);
-      skip = bound < (long long)pb;
+      skip = bound < (long long)prune_seen;
     }
 
     if (skip) {
