@@ -113,6 +113,16 @@ __device__ __forceinline__ int ld_relaxed(const int32_t* p) {
   return v;
 }
 
+// Spin until *p >= need with exponential back-off: a waiting warp shares its
+// SM sub-partition with a computing one, so it must not steal issue slots.
+__device__ __forceinline__ void wait_progress(const int32_t* p, int need) {
+  unsigned ns = 32;
+  while (ld_relaxed(p) < need) {
+    __nanosleep(ns);
+    ns = ns < 4096 ? ns * 2 : 4096;
+  }
+}
+
 // Border values, engine.py:340-401.  I is a DP row, J a DP column.
 __device__ __forceinline__ int left_h(int border, int I, int go, int ge) {
   switch (border) {
@@ -227,7 +237,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
   } else if (s == 0) {
     diag = top_h(J.border, cb, go, ge) - goe;
   } else if (cb - 1 >= cbp && cb - 1 < cep) {
-    while (ld_relaxed(up_progress) < cb) __nanosleep(20);
+    wait_progress(up_progress, cb);
     fence_acq_rel();
     diag = __ldcg(inbuf + (cb - 1)).x;
   } else {
@@ -347,7 +357,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
             const long long tw = clock64();
             unsigned long long a0, a1;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a0));
-            while (ld_relaxed(up_progress) < need) __nanosleep(20);
+            wait_progress(up_progress, need);
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a1));
             gw += a1 - a0;
             wait_cycles += clock64() - tw;

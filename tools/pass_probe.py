@@ -40,6 +40,8 @@ for spec in sys.argv[1:]:
         ctx.set_option("reset_debug", 0)
         res = S.run(sp)[0]
         dbg = ctx.debug_stats()
+        tm = ctx.debug_times()
+        np.save(ROOT / "gpurun_out" / f"times_{spec.replace(':', '_').replace('=', '')}.npy", tm)
     print(json.dumps({"spec": spec, "kernel_ms": round(res.kernel_ms, 2),
                       "cells": res.cells_executed,
                       "gcups_exec": round(res.cells_executed / res.kernel_ms / 1e6, 1),
