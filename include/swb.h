@@ -102,6 +102,19 @@ typedef struct {
   int32_t want_final_rows;  /* fill final_row_h/f (PassResult, engine.py:120-131) */
   int64_t* final_row_h;     /* caller-owned int64[len2 + 1] or NULL */
   int64_t* final_row_f;     /* sentinel-derived values are reported <= SWB_NEG_REPORT */
+  /* Row slab of a pass split across GPUs; all zero for a whole pass.
+   * row_offset: DP row of this slab's first row (left border, reported best_i).
+   * ext_in_*:  device pointers (local memory, written by the GPU above through
+   *            peer mapping) holding the bottom DP row (H-go-ge, F) of the slab
+   *            above and its column progress counter; replaces the top border.
+   * ext_out_*: device pointers (peer memory of the GPU below) receiving this
+   *            slab's bottom row and progress.  Slab rows must be a multiple of
+   *            32 x rows_per_lane except for the last slab; no band. */
+  int64_t row_offset;
+  uint64_t ext_in_buf;
+  uint64_t ext_in_progress;
+  uint64_t ext_out_buf;
+  uint64_t ext_out_progress;
 } swb_pass_desc;
 
 /* PassResult (engine.py:120-131) minus the final rows (written in place). */
@@ -213,6 +226,17 @@ int32_t swb_timer_stop(swb_ctx* ctx, double* ms);
 /* Overwrite `bytes` (0: 512 MiB, > the 126 MB L2) of scratch on the stream to
  * evict earlier working sets from L2 between timed steps. */
 int32_t swb_flush_l2(swb_ctx* ctx, int64_t bytes);
+
+/* --- multi-GPU boundary rows ------------------------------------
+ * A boundary is int2[n2] + one int32 progress counter in device memory of the
+ * consuming GPU.  Export/import turn it into a peer pointer for the producing
+ * GPU's process (CUDA IPC over NVLink). */
+int32_t swb_boundary_alloc(swb_ctx* ctx, int64_t n2, uint64_t* buf, uint64_t* progress);
+int32_t swb_boundary_reset(swb_ctx* ctx, uint64_t progress);
+int32_t swb_boundary_free(swb_ctx* ctx, uint64_t buf, uint64_t progress);
+int32_t swb_ipc_export(swb_ctx* ctx, uint64_t ptr, uint8_t* handle64);
+int32_t swb_ipc_import(swb_ctx* ctx, const uint8_t* handle64, uint64_t* ptr);
+int32_t swb_ipc_close(swb_ctx* ctx, uint64_t ptr);
 
 /* Device-side timing of the most recent swb_pass launch (ms, CUDA events). */
 double swb_last_kernel_ms(swb_ctx* ctx);

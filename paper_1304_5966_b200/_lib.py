@@ -36,7 +36,10 @@ class PassDesc(ctypes.Structure):
                 ("off2", c_i64), ("len2", c_i64), ("rev1", c_i32), ("rev2", c_i32),
                 ("border", c_i32), ("clamp_zero", c_i32), ("track", c_i32), ("has_band", c_i32),
                 ("band_lo", c_i64), ("band_hi", c_i64), ("prune", c_i32),
-                ("want_final_rows", c_i32), ("final_row_h", c_p), ("final_row_f", c_p)]
+                ("want_final_rows", c_i32), ("final_row_h", c_p), ("final_row_f", c_p),
+                ("row_offset", c_i64), ("ext_in_buf", ctypes.c_uint64),
+                ("ext_in_progress", ctypes.c_uint64), ("ext_out_buf", ctypes.c_uint64),
+                ("ext_out_progress", ctypes.c_uint64)]
 
 
 class PassOut(ctypes.Structure):
@@ -68,6 +71,8 @@ EXPORTS = (
     "swb_seq_release", "swb_pass", "swb_crossings", "swb_leaves", "swb_measure_int_peak",
     "swb_last_kernel_ms", "swb_launch_count", "swb_set_option", "swb_debug_stats",
     "swb_debug_times", "swb_timer_start", "swb_timer_stop", "swb_flush_l2",
+    "swb_boundary_alloc", "swb_boundary_reset", "swb_boundary_free", "swb_ipc_export",
+    "swb_ipc_import", "swb_ipc_close",
 )
 
 _lib = None
@@ -122,6 +127,19 @@ def load() -> ctypes.CDLL:
         lib.swb_timer_stop.restype = c_i32
         lib.swb_flush_l2.argtypes = [c_p, c_i64]
         lib.swb_flush_l2.restype = c_i32
+        u64, P64 = ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)
+        lib.swb_boundary_alloc.argtypes = [c_p, c_i64, P64, P64]
+        lib.swb_boundary_alloc.restype = c_i32
+        lib.swb_boundary_reset.argtypes = [c_p, u64]
+        lib.swb_boundary_reset.restype = c_i32
+        lib.swb_boundary_free.argtypes = [c_p, u64, u64]
+        lib.swb_boundary_free.restype = c_i32
+        lib.swb_ipc_export.argtypes = [c_p, u64, c_p]
+        lib.swb_ipc_export.restype = c_i32
+        lib.swb_ipc_import.argtypes = [c_p, c_p, P64]
+        lib.swb_ipc_import.restype = c_i32
+        lib.swb_ipc_close.argtypes = [c_p, u64]
+        lib.swb_ipc_close.restype = c_i32
         _lib = lib
         return lib
 

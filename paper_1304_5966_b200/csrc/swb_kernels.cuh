@@ -63,6 +63,12 @@ struct JobDev {
   unsigned long long* counters;  // [0] cells, [1] blocks executed, [2] blocks pruned,
                                  // [3] cycles spent waiting on the strip above, [4] strip cycles
   int32_t* prune_best;   // running best score (plain) for pruning
+  int32_t row_offset;    // DP row of row 0 (row slab of a multi-GPU pass)
+  int32_t pad1;
+  int2* ext_in;          // strip 0 top input from the GPU above (null: top border)
+  int32_t* ext_in_prog;
+  int2* ext_out;         // last strip bottom row to the GPU below (null: local buffer)
+  int32_t* ext_out_prog;
 };
 
 struct PassParams {
@@ -103,6 +109,22 @@ __device__ __forceinline__ void st_release(int32_t* p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ int ld_acquire_sys(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys(int32_t* p, int v) {
+  asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ int ld_relaxed_sys(const int32_t* p) {
+  int v;
+  asm volatile("ld.relaxed.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void fence_acq_rel() {
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
@@ -115,9 +137,9 @@ __device__ __forceinline__ int ld_relaxed(const int32_t* p) {
 
 // Spin until *p >= need with exponential back-off: a waiting warp shares its
 // SM sub-partition with a computing one, so it must not steal issue slots.
-__device__ __forceinline__ void wait_progress(const int32_t* p, int need) {
+__device__ __forceinline__ void wait_progress(const int32_t* p, int need, bool sys = false) {
   unsigned ns = 32;
-  while (ld_relaxed(p) < need) {
+  while ((sys ? ld_relaxed_sys(p) : ld_relaxed(p)) < need) {
     __nanosleep(ns);
     ns = ns < 4096 ? ns * 2 : 4096;
   }
@@ -201,10 +223,26 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
   int2* __restrict__ outbuf = J.buf[s & 1];
   int32_t* my_progress = J.progress + s;
   const int32_t* up_progress = s > 0 ? J.progress + (s - 1) : nullptr;
+  // multi-GPU row slab: strip 0 consumes the slab above (another GPU), the
+  // last strip produces into the slab below (peer memory); sys-scope ordering
+  const bool ext_in = (s == 0) && (J.ext_in != nullptr);
+  const bool ext_out = (s == J.nstrips - 1) && (J.ext_out != nullptr);
+  const bool first = (s == 0) && !ext_in;  // top border of the whole pass
+  if (ext_in) {
+    inbuf = J.ext_in;
+    up_progress = J.ext_in_prog;
+    cbp = 0;
+    cep = n2;
+  }
+  if (ext_out) {
+    outbuf = J.ext_out;
+    my_progress = J.ext_out_prog;
+  }
 
   if (cb >= ce) {
     if (lane == 0) {
-      st_release(my_progress, 0x7fffffff);
+      if (ext_out) st_release_sys(my_progress, 0x7fffffff);
+      else st_release(my_progress, 0x7fffffff);
       J.strip_res[s] = make_int4(0, -1, -1, 0);
     }
     return;
@@ -224,21 +262,22 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     H2[r] = 0;
-    const int hl = (cb == 0) ? left_h(J.border, lrow0 + r + 1, go, ge) - goe : fillm;
+    const int hl = (cb == 0) ? left_h(J.border, J.row_offset + lrow0 + r + 1, go, ge) - goe : fillm;
     H[r] = hl;
     E[r] = vmaxadd(SWB_NEG32, -ge, hl);
   }
   // Diagonal for row 0 at column cb: H(lrow0 - 1, cb - 1).
   int diag;
   if (cb == 0) {
-    diag = left_h(J.border, lrow0, go, ge) - goe;
+    diag = left_h(J.border, J.row_offset + lrow0, go, ge) - goe;
   } else if (lane != 0) {
     diag = fillm;
-  } else if (s == 0) {
+  } else if (first) {
     diag = top_h(J.border, cb, go, ge) - goe;
   } else if (cb - 1 >= cbp && cb - 1 < cep) {
-    wait_progress(up_progress, cb);
-    fence_acq_rel();
+    wait_progress(up_progress, cb, ext_in);
+    if (ext_in) (void)ld_acquire_sys(up_progress);
+    else fence_acq_rel();
     diag = __ldcg(inbuf + (cb - 1)).x;
   } else {
     diag = fillm;
@@ -350,24 +389,24 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
         const int cn = c + 32;
         code_next = (cn < ce) ? (int)J.cols[(long long)cn * J.cstep] : 0;
       }
-      if (s > 0 && s0 < cep && s0 + 32 > cbp) {
+      if (!first && s0 < cep && s0 + 32 > cbp) {
         const int need = (s0 + 32 < cep) ? s0 + 32 : cep;
         if (known_prog < need) {
-          if (ld_relaxed(up_progress) < need) {
+          if ((ext_in ? ld_relaxed_sys(up_progress) : ld_relaxed(up_progress)) < need) {
             const long long tw = clock64();
             unsigned long long a0, a1;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a0));
-            wait_progress(up_progress, need);
+            wait_progress(up_progress, need, ext_in);
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a1));
             gw += a1 - a0;
             wait_cycles += clock64() - tw;
           }
-          known_prog = ld_acquire(up_progress);
+          known_prog = ext_in ? ld_acquire_sys(up_progress) : ld_acquire(up_progress);
         }
       }
       if (c < ce) {
         int th, tf;
-        if (s == 0) {
+        if (first) {
           th = top_h(J.border, c + 1, go, ge) - goe;
           tf = SWB_NEG32;
         } else if (c >= cbp && c < cep) {
@@ -441,13 +480,17 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     {
       const int c = s0 - 31 + lane;
       if (c >= cb && c < ce) __stcg(outbuf + c, sm->out[lane]);
-      if (P.proto == 0) __threadfence();
+      if (ext_out) __threadfence_system();
+      else if (P.proto == 0) __threadfence();
       else if (P.proto == 1) fence_acq_rel();
       __syncwarp();
       if (lane == 0) {
         int pub = s0 + 1;
         if (pub > ce) pub = ce;
-        if (pub >= cb) st_release(my_progress, pub);
+        if (pub >= cb) {
+          if (ext_out) st_release_sys(my_progress, pub);
+          else st_release(my_progress, pub);
+        }
       }
     }
 
@@ -457,7 +500,10 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       if (lane == 0 && bm > -goe) atomicMax(J.prune_best, bm + goe);
     }
   }
-  if (lane == 0) st_release(my_progress, ce);
+  if (lane == 0) {
+    if (ext_out) st_release_sys(my_progress, ce);
+    else st_release(my_progress, ce);
+  }
 
   // Strip result: decode the key, then warp reduction with the mode's tie
   // rule (engine.py:247-259).

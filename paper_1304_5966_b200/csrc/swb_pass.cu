@@ -252,11 +252,12 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     order[q] = (int)q;
     PassReq& r = reqs[q];
     if (r.n1 < 1 || r.n2 < 1) return swb_fail(SWB_EINVAL, "cannot tile an empty matrix");
-    int rc = swb_check_range(sc, r.n1, r.n2);
+    int rc = swb_check_range(sc, r.row_offset + r.n1, r.n2);
     if (rc) return rc;
     // tracked passes fold H and the row rank into one int32 key (H * 32 + rank)
     if (r.track != kTrackNone &&
-        (long long)std::max(sc.max_sub, 0) * std::min(r.n1, r.n2) + sc.goe >= (1LL << 26) - 64)
+        (long long)std::max(sc.max_sub, 0) * std::min<long long>(r.row_offset + r.n1, r.n2) +
+                sc.goe >= (1LL << 26) - 64)
       return swb_fail(SWB_ERANGE, "tracked pass %d x %d exceeds the 26-bit score key range",
                       r.n1, r.n2);
   }
@@ -275,6 +276,11 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     }
     a = b;
   }
+  for (const PassReq& r : reqs)
+    if (r.ext_out && r.n1 % (32 * r.R) != 0)
+      return swb_fail(SWB_EINVAL,
+                      "row slab of %d rows feeding another slab must be a multiple of 32 x %d "
+                      "(set rows_per_lane)", r.n1, r.R);
   auto key = [&](int q) { return cls(q) * 1000 + reqs[q].R; };
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return key(a) < key(b); });
 
@@ -343,6 +349,11 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
         J.band_hi = (int32_t)hi;
       }
       J.prune = r.prune ? 1 : 0;
+      J.row_offset = (int32_t)r.row_offset;
+      J.ext_in = r.ext_in;
+      J.ext_in_prog = r.ext_in_prog;
+      J.ext_out = r.ext_out;
+      J.ext_out_prog = r.ext_out_prog;
       J.nstrips = r.nstrips;
       J.want_final = r.want_final ? 1 : 0;
       J.item_base = item;
@@ -463,7 +474,7 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
         bs = SWB_NEG_INF_REF + (bs - (long long)SWB_NEG32);
       }
       r.best_score = bs;
-      r.best_i = bi;
+      r.best_i = bi >= 0 ? bi + r.row_offset : bi;
       r.best_j = bj;
       r.cells = (long long)h_cnt[5 * t + 0];
       r.blocks_exec = (long long)h_cnt[5 * t + 1];
@@ -563,6 +574,18 @@ extern "C" int32_t swb_pass(swb_ctx* ctx, const swb_scheme* scheme, const swb_pa
     if (r.want_final && (!d.final_row_h || !d.final_row_f))
       return swb_fail(SWB_EINVAL, "want_final_rows needs final_row_h/final_row_f");
     r.force_R = ctx->force_R;
+    r.row_offset = d.row_offset;
+    r.ext_in = reinterpret_cast<int2*>(d.ext_in_buf);
+    r.ext_in_prog = reinterpret_cast<int32_t*>(d.ext_in_progress);
+    r.ext_out = reinterpret_cast<int2*>(d.ext_out_buf);
+    r.ext_out_prog = reinterpret_cast<int32_t*>(d.ext_out_progress);
+    if ((r.ext_in || r.ext_out || r.row_offset) && r.has_band)
+      return swb_fail(SWB_EUNSUPPORTED, "row slabs (multi-GPU) do not support a band");
+    if ((r.ext_in == nullptr) != (r.ext_in_prog == nullptr) ||
+        (r.ext_out == nullptr) != (r.ext_out_prog == nullptr))
+      return swb_fail(SWB_EINVAL, "ext boundary needs both a buffer and a progress counter");
+    if (r.row_offset < 0 || r.row_offset + r.n1 >= (1LL << 31))
+      return swb_fail(SWB_ERANGE, "row_offset out of range");
   }
   double ms = 0.0;
   rc = swb_run_passes(ctx, sc, reqs, &ms);
@@ -595,6 +618,61 @@ extern "C" int32_t swb_pass(swb_ctx* ctx, const swb_scheme* scheme, const swb_pa
       }
     }
   }
+  SWB_API_END();
+}
+
+extern "C" int32_t swb_boundary_alloc(swb_ctx* ctx, int64_t n2, uint64_t* buf, uint64_t* progress) {
+  SWB_API_BEGIN(ctx);
+  if (n2 < 1 || !buf || !progress) return swb_fail(SWB_EINVAL, "bad arguments");
+  void* b = nullptr;
+  void* p = nullptr;
+  SWB_CUDA(cudaMalloc(&b, sizeof(int2) * (size_t)n2));
+  SWB_CUDA(cudaMalloc(&p, 256));
+  SWB_CUDA(cudaMemset(p, 0, 256));
+  *buf = reinterpret_cast<uint64_t>(b);
+  *progress = reinterpret_cast<uint64_t>(p);
+  SWB_API_END();
+}
+
+extern "C" int32_t swb_boundary_reset(swb_ctx* ctx, uint64_t progress) {
+  SWB_API_BEGIN(ctx);
+  SWB_CUDA(cudaMemsetAsync(reinterpret_cast<void*>(progress), 0, sizeof(int32_t), ctx->stream));
+  SWB_CUDA(cudaStreamSynchronize(ctx->stream));
+  SWB_API_END();
+}
+
+extern "C" int32_t swb_boundary_free(swb_ctx* ctx, uint64_t buf, uint64_t progress) {
+  SWB_API_BEGIN(ctx);
+  SWB_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (buf) SWB_CUDA(cudaFree(reinterpret_cast<void*>(buf)));
+  if (progress) SWB_CUDA(cudaFree(reinterpret_cast<void*>(progress)));
+  SWB_API_END();
+}
+
+extern "C" int32_t swb_ipc_export(swb_ctx* ctx, uint64_t ptr, uint8_t* handle64) {
+  SWB_API_BEGIN(ctx);
+  if (!ptr || !handle64) return swb_fail(SWB_EINVAL, "bad arguments");
+  cudaIpcMemHandle_t h;
+  SWB_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(ptr)));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  memcpy(handle64, &h, 64);
+  SWB_API_END();
+}
+
+extern "C" int32_t swb_ipc_import(swb_ctx* ctx, const uint8_t* handle64, uint64_t* ptr) {
+  SWB_API_BEGIN(ctx);
+  if (!ptr || !handle64) return swb_fail(SWB_EINVAL, "bad arguments");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, 64);
+  void* p = nullptr;
+  SWB_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  *ptr = reinterpret_cast<uint64_t>(p);
+  SWB_API_END();
+}
+
+extern "C" int32_t swb_ipc_close(swb_ctx* ctx, uint64_t ptr) {
+  SWB_API_BEGIN(ctx);
+  if (ptr) SWB_CUDA(cudaIpcCloseMemHandle(reinterpret_cast<void*>(ptr)));
   SWB_API_END();
 }
 

@@ -25,6 +25,11 @@ struct PassReq {
   int32_t* fin_h_dev = nullptr;  // device int32[n2] (cell columns); allocated if null
   int32_t* fin_f_dev = nullptr;
   int force_R = 0;
+  long long row_offset = 0;
+  int2* ext_in = nullptr;
+  int32_t* ext_in_prog = nullptr;
+  int2* ext_out = nullptr;
+  int32_t* ext_out_prog = nullptr;
   // filled by swb_run_passes
   int R = 0;
   int nstrips = 0;

@@ -223,8 +223,11 @@ class Session:
         return False
 
     def desc(self, rows: tuple, cols: tuple, border: str, clamp: bool, track: int,
-             band=None, prune=False, final=None) -> _lib.PassDesc:
-        """rows/cols = (offset, length, reversed) slices of seq1/seq2."""
+             band=None, prune=False, final=None, row_offset=0, ext_in=None,
+             ext_out=None) -> _lib.PassDesc:
+        """rows/cols = (offset, length, reversed) slices of seq1/seq2;
+        row_offset/ext_in/ext_out describe a row slab of a multi-GPU pass
+        (multigpu.py, include/swb.h)."""
         d = _lib.PassDesc()
         d.seq1, d.seq2 = self.s1, self.s2
         d.off1, d.len1, d.rev1 = int(rows[0]), int(rows[1]), int(rows[2])
@@ -239,6 +242,11 @@ class Session:
             d.want_final_rows = 1
             d.final_row_h = final[0].ctypes.data
             d.final_row_f = final[1].ctypes.data
+        d.row_offset = int(row_offset)
+        if ext_in is not None:
+            d.ext_in_buf, d.ext_in_progress = int(ext_in[0]), int(ext_in[1])
+        if ext_out is not None:
+            d.ext_out_buf, d.ext_out_progress = int(ext_out[0]), int(ext_out[1])
         return d
 
     def run(self, specs: list[dict]) -> list[PassResult]:

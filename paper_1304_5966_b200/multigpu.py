@@ -15,6 +15,8 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 TRACK_NONE, TRACK_MIN, TRACK_MAX = 0, 1, 2
+SLAB_ROWS_PER_LANE = 32  # every rank uses the same strip height: 32 lanes x 32 rows
+SLAB_STRIP_ROWS = 32 * SLAB_ROWS_PER_LANE
 
 
 @dataclass(frozen=True)
@@ -74,3 +76,80 @@ def merge_best(results: list[tuple[int, int, int]], track: int) -> tuple[int, in
 def handoff_bytes(n2: int) -> int:
     """Bytes one slab boundary moves over NVLink: (H, F) int32 per column."""
     return 8 * n2
+
+
+# -- device path ------------------------------------------------------------------
+
+class Boundary:
+    """Incoming boundary row of one GPU: int2[n2] + progress counter in its own
+    device memory (written by the GPU above through a peer mapping)."""
+
+    def __init__(self, ctx, n2: int):
+        import ctypes
+        from . import _lib
+        self.ctx = ctx
+        b, p = ctypes.c_uint64(), ctypes.c_uint64()
+        _lib.check(ctx.lib.swb_boundary_alloc(ctx.ptr, int(n2), ctypes.byref(b), ctypes.byref(p)),
+                   "swb_boundary_alloc")
+        self.buf, self.progress = int(b.value), int(p.value)
+
+    def reset(self):
+        from . import _lib
+        _lib.check(self.ctx.lib.swb_boundary_reset(self.ctx.ptr, self.progress),
+                   "swb_boundary_reset")
+
+    def export(self) -> tuple[bytes, bytes]:
+        return ipc_export(self.ctx, self.buf), ipc_export(self.ctx, self.progress)
+
+    def free(self):
+        from . import _lib
+        _lib.check(self.ctx.lib.swb_boundary_free(self.ctx.ptr, self.buf, self.progress),
+                   "swb_boundary_free")
+        self.buf = self.progress = 0
+
+
+def ipc_export(ctx, ptr: int) -> bytes:
+    import ctypes
+    from . import _lib
+    h = (ctypes.c_uint8 * 64)()
+    _lib.check(ctx.lib.swb_ipc_export(ctx.ptr, int(ptr), h), "swb_ipc_export")
+    return bytes(h)
+
+
+def ipc_import(ctx, handle: bytes) -> int:
+    import ctypes
+    from . import _lib
+    h = (ctypes.c_uint8 * 64).from_buffer_copy(handle)
+    p = ctypes.c_uint64()
+    _lib.check(ctx.lib.swb_ipc_import(ctx.ptr, h, ctypes.byref(p)), "swb_ipc_import")
+    return int(p.value)
+
+
+def slab_spec(slab: Slab, n2: int, ext_in: tuple[int, int] | None,
+              ext_out: tuple[int, int] | None, prune: bool = True) -> dict:
+    """Session.run() spec of one slab of a local score pass (phase1.py:44-85)."""
+    return dict(rows=(slab.row0, slab.rows, 0), cols=(0, n2, 0), border="local", clamp=True,
+                track=TRACK_MIN, prune=prune, row_offset=slab.row0,
+                ext_in=ext_in, ext_out=ext_out)
+
+
+def run_slabs_sequential(S, slabs: list[Slab], prune: bool = True):
+    """One-GPU validation of the slab handoff: run the slabs of a score pass one
+    after another on the same device, each consuming the previous slab's
+    boundary row through the ext_in/ext_out path (no concurrent waiting).
+    Returns the merged (score, i, j) and the per-slab results."""
+    bounds = [Boundary(S.ctx, S.n2) for _ in slabs[1:]]
+    S.ctx.set_option("rows_per_lane", SLAB_ROWS_PER_LANE)
+    try:
+        results = []
+        for g, slab in enumerate(slabs):
+            ext_in = (bounds[g - 1].buf, bounds[g - 1].progress) if g > 0 else None
+            ext_out = (bounds[g].buf, bounds[g].progress) if g + 1 < len(slabs) else None
+            r = S.run([slab_spec(slab, S.n2, ext_in, ext_out, prune)])[0]
+            results.append(r)
+        merged = merge_best([(r.best_score, r.best_i, r.best_j) for r in results], TRACK_MIN)
+        return merged, results
+    finally:
+        S.ctx.set_option("rows_per_lane", 0)
+        for b in bounds:
+            b.free()
