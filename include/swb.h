@@ -98,7 +98,11 @@ typedef struct {
   int32_t has_band;   /* admissible (row - col) interval [band_lo, band_hi] */
   int64_t band_lo;
   int64_t band_hi;
-  int32_t prune;            /* phase-1 upper-bound pruning (phase1.py:55-59) */
+  int32_t prune;            /* 0 off; 1 phase-1 running-best bound (phase1.py:55-59, local);
+                               2 fixed target (restricted search: no path through a skipped
+                                 block reaches prune_target); 3 target at corner (no path
+                                 through a skipped block reaches DP (corner_i, corner_j)
+                                 with score prune_target) */
   int32_t want_final_rows;  /* fill final_row_h/f (PassResult, engine.py:120-131) */
   int64_t* final_row_h;     /* caller-owned int64[len2 + 1] or NULL */
   int64_t* final_row_f;     /* sentinel-derived values are reported <= SWB_NEG_REPORT */
@@ -111,6 +115,9 @@ typedef struct {
    *            slab's bottom row and progress.  Slab rows must be a multiple of
    *            32 x rows_per_lane except for the last slab; no band. */
   int64_t row_offset;
+  int64_t prune_target;
+  int64_t corner_i;
+  int64_t corner_j;
   uint64_t ext_in_buf;
   uint64_t ext_in_progress;
   uint64_t ext_out_buf;

@@ -37,7 +37,8 @@ class PassDesc(ctypes.Structure):
                 ("border", c_i32), ("clamp_zero", c_i32), ("track", c_i32), ("has_band", c_i32),
                 ("band_lo", c_i64), ("band_hi", c_i64), ("prune", c_i32),
                 ("want_final_rows", c_i32), ("final_row_h", c_p), ("final_row_f", c_p),
-                ("row_offset", c_i64), ("ext_in_buf", ctypes.c_uint64),
+                ("row_offset", c_i64), ("prune_target", c_i64), ("corner_i", c_i64),
+                ("corner_j", c_i64), ("ext_in_buf", ctypes.c_uint64),
                 ("ext_in_progress", ctypes.c_uint64), ("ext_out_buf", ctypes.c_uint64),
                 ("ext_out_progress", ctypes.c_uint64)]
 

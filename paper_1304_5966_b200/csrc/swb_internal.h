@@ -44,6 +44,7 @@ struct swb_ctx {
   int proto = 2;
   int claim_mode = 0;
   bool trace = false;
+  int mm_prune = 1;
   std::vector<unsigned long long> dbg_times;
   // scratch
   swb_buf jobs, rowbuf, progress, results, finals, misc, host_pinned, flush;

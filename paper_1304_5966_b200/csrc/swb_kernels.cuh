@@ -50,7 +50,9 @@ struct JobDev {
   int32_t border;
   int32_t fill_h;  // H written into skipped cells: 0 (local) or NEG
   int32_t has_band, band_lo, band_hi;
-  int32_t prune;
+  int32_t prune;         // 0 off, 1 running best (local), 2 fixed target, 3 target at corner
+  int32_t prune_target;
+  int32_t corner_i, corner_j;  // DP corner the path must reach (prune kind 3)
   int32_t nstrips;
   int32_t want_final;
   int64_t item_base;
@@ -384,7 +386,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     {
       const int c = s0 + lane;
       const int code = code_next;
-      const int pb_now = (LOCAL && J.prune) ? ld_relaxed(J.prune_best) : 0;
+      const int pb_now = (LOCAL && J.prune == 1) ? ld_relaxed(J.prune_best) : 0;
       {
         const int cn = c + 32;
         code_next = (cn < ce) ? (int)J.cols[(long long)cn * J.cstep] : 0;
@@ -425,35 +427,59 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     const bool steady = (s0 - 31 >= cb) && (s0 + 32 <= ce);
 
     // (2) pruning: skip the whole 32-step block when no path through it can
-    // reach the running best (phase1.py:24-41, :55-59; strict inequality).
+    // matter.  kind 1 (phase 1): cannot reach the running best
+    // (phase1.py:24-41, :55-59; strict); kind 2 (restricted search): cannot
+    // reach the known target anywhere; kind 3 (Myers-Miller halves): cannot be
+    // on a path that reaches the subproblem's end corner with the expected
+    // score.  Skipped cells get the fill of engine.py:286-293.
     bool skip = false;
-    if (LOCAL && J.prune && steady) {
+    if (J.prune && steady) {
       int m = out_hm > diag ? out_hm : diag;
 #pragma unroll
       for (int r = 0; r < R; ++r) m = m > H[r] ? m : H[r];
       const int tv = sm->ring[(s0 + lane) & 63].x;
       m = m > tv ? m : tv;
       m = __reduce_max_sync(0xffffffffu, m);
-      const int inmax = m + goe > 0 ? m + goe : 0;
+      const long long inm = (long long)m + goe;
       const int rem_r = n1 - R0;
       const int rem_c = n2 - (s0 - 31);
-      const long long bound =
-          (long long)inmax + (long long)P.max_sub * (long long)(rem_r < rem_c ? rem_r : rem_c);
-      skip = bound < (long long)prune_seen;
+      const long long ms = P.max_sub;
+      if (J.prune == 1) {
+        const long long bound = (inm > 0 ? inm : 0) + ms * (long long)(rem_r < rem_c ? rem_r : rem_c);
+        skip = bound < (long long)prune_seen;
+      } else if (J.prune == 2) {
+        const long long bound = inm + ms * (long long)(rem_r < rem_c ? rem_r : rem_c);
+        skip = bound < (long long)J.prune_target;
+      } else {
+        int i_hi = R0 + 32 * R;
+        if (i_hi > n1) i_hi = n1;
+        const long long di_max = (long long)J.corner_i - (R0 + 1);
+        const long long dj_max = (long long)J.corner_j - (s0 - 31 + 1);
+        const long long off = (long long)J.corner_i - J.corner_j;
+        const long long dlo = off - ((long long)(i_hi - 1) - (s0 - 31));
+        const long long dhi = off - ((long long)R0 - (s0 + 31));
+        long long k = 0;
+        if (dlo > 0) k = dlo;
+        else if (dhi < 0) k = -dhi;
+        const long long ub = ms * (di_max < dj_max ? di_max : dj_max) - (k > 0 ? go + (long long)ge * k : 0);
+        // + 2 go + ge: a completion may continue an open gap, and the two
+        // halves of a gap join each charge one opening fee
+        skip = inm + ub + 2LL * go + ge < (long long)J.prune_target;
+      }
     }
 
     if (skip) {
       ++pruned_blocks;
-      const int negE = vmaxadd(SWB_NEG32, -ge, -goe);
+      const int negE = vmaxadd(SWB_NEG32, -ge, fillm);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        H[r] = -goe;
+        H[r] = fillm;
         E[r] = negE;
       }
-      diag = (lane == 0) ? sm->ring[(s0 + 31) & 63].x : -goe;
-      out_hm = -goe;
+      diag = (lane == 0) ? sm->ring[(s0 + 31) & 63].x : fillm;
+      out_hm = fillm;
       out_f = SWB_NEG32;
-      sm->out[lane] = make_int2(-goe, SWB_NEG32);
+      sm->out[lane] = make_int2(fillm, SWB_NEG32);
       __syncwarp();
     } else {
       ++exec_blocks;
@@ -495,7 +521,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     }
 
     // (5) running best for pruning (monotone, never ahead of the truth).
-    if (LOCAL && J.prune && TRACK == kTrackMin) {
+    if (LOCAL && J.prune == 1 && TRACK == kTrackMin) {
       const int bm = __reduce_max_sync(0xffffffffu, bkey >> 5);
       if (lane == 0 && bm > -goe) atomicMax(J.prune_best, bm + goe);
     }

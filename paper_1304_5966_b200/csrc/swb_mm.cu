@@ -405,6 +405,14 @@ extern "C" int32_t swb_crossings(swb_ctx* ctx, const swb_scheme* scheme, int32_t
     dn.fin_h_dev = fin + off + 2 * cols;
     dn.fin_f_dev = fin + off + 3 * cols;
     up.force_R = dn.force_R = ctx->force_R;
+    if (ctx->mm_prune) {
+      // only cells that can still lie on a path of the expected score to the
+      // far corner matter for the crossing (prune kind 3)
+      up.prune = dn.prune = 3;
+      up.prune_target = dn.prune_target = s.expected;
+      up.corner_i = dn.corner_i = rows;
+      up.corner_j = dn.corner_j = cols;
+    }
     CombineDev& c = comb[t];
     c.uh = up.fin_h_dev;
     c.uf = up.fin_f_dev;

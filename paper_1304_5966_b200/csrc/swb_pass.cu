@@ -348,7 +348,11 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
         J.band_lo = (int32_t)lo;
         J.band_hi = (int32_t)hi;
       }
-      J.prune = r.prune ? 1 : 0;
+      J.prune = r.prune;
+      J.prune_target = (int32_t)std::max<long long>(std::min<long long>(r.prune_target, 1LL << 29),
+                                                    -(1LL << 29));
+      J.corner_i = (int32_t)r.corner_i;
+      J.corner_j = (int32_t)r.corner_j;
       J.row_offset = (int32_t)r.row_offset;
       J.ext_in = r.ext_in;
       J.ext_in_prog = r.ext_in_prog;
@@ -519,6 +523,10 @@ extern "C" int32_t swb_set_option(swb_ctx* ctx, const char* name, int64_t value)
     ctx->max_ctas_per_sm = (int)value;
     return SWB_OK;
   }
+  if (!strcmp(name, "mm_prune")) {
+    ctx->mm_prune = (int)value;
+    return SWB_OK;
+  }
   if (!strcmp(name, "claim_mode")) {
     ctx->claim_mode = (int)value;  // 0 auto, 1 force CTA claiming, 2 force warp claiming
     return SWB_OK;
@@ -565,11 +573,16 @@ extern "C" int32_t swb_pass(swb_ctx* ctx, const swb_scheme* scheme, const swb_pa
     r.track = d.track;
     if (r.local && (d.border != SWB_BORDER_LOCAL || d.track != SWB_TRACK_MIN || d.has_band))
       return swb_fail(SWB_EUNSUPPORTED, "clamped passes must use local borders, TRACK_MIN, no band");
-    if (!r.local && d.prune) return swb_fail(SWB_EUNSUPPORTED, "pruning needs a local pass");
+    if (d.prune < 0 || d.prune > 3) return swb_fail(SWB_EINVAL, "bad prune kind %d", d.prune);
+    if (r.local && d.prune > 1) return swb_fail(SWB_EUNSUPPORTED, "local passes prune on the running best");
+    if (!r.local && d.prune == 1) return swb_fail(SWB_EUNSUPPORTED, "running-best pruning needs a local pass");
     r.has_band = d.has_band != 0;
     r.band_lo = d.band_lo;
     r.band_hi = d.band_hi;
-    r.prune = d.prune != 0;
+    r.prune = d.prune;
+    r.prune_target = d.prune_target;
+    r.corner_i = d.corner_i;
+    r.corner_j = d.corner_j;
     r.want_final = d.want_final_rows != 0;
     if (r.want_final && (!d.final_row_h || !d.final_row_f))
       return swb_fail(SWB_EINVAL, "want_final_rows needs final_row_h/final_row_f");

@@ -20,7 +20,9 @@ struct PassReq {
   int track = 0;
   bool has_band = false;
   long long band_lo = 0, band_hi = 0;
-  bool prune = false;
+  int prune = 0;  // 0 off, 1 running best, 2 fixed target, 3 target at corner
+  long long prune_target = 0;
+  long long corner_i = 0, corner_j = 0;
   bool want_final = false;
   int32_t* fin_h_dev = nullptr;  // device int32[n2] (cell columns); allocated if null
   int32_t* fin_f_dev = nullptr;

@@ -208,6 +208,7 @@ class Session:
         self.s2 = ctx.upload(codes2)
         self.kernel_ms = 0.0
         self.cells = 0
+        self.target_prune = True  # phase-2 restricted searches skip hopeless blocks
 
     def close(self):
         if self.s1 is not None:
@@ -224,7 +225,7 @@ class Session:
 
     def desc(self, rows: tuple, cols: tuple, border: str, clamp: bool, track: int,
              band=None, prune=False, final=None, row_offset=0, ext_in=None,
-             ext_out=None) -> _lib.PassDesc:
+             ext_out=None, prune_target=0, corner=None) -> _lib.PassDesc:
         """rows/cols = (offset, length, reversed) slices of seq1/seq2;
         row_offset/ext_in/ext_out describe a row slab of a multi-GPU pass
         (multigpu.py, include/swb.h)."""
@@ -237,7 +238,10 @@ class Session:
         d.track = int(track)
         if band is not None:
             d.has_band, d.band_lo, d.band_hi = 1, int(band[0]), int(band[1])
-        d.prune = int(prune)
+        d.prune = int(prune)  # True -> 1 (running best); 2 / 3 target kinds
+        d.prune_target = int(prune_target)
+        if corner is not None:
+            d.corner_i, d.corner_j = int(corner[0]), int(corner[1])
         if final is not None:
             d.want_final_rows = 1
             d.final_row_h = final[0].ctypes.data

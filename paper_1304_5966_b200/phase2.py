@@ -72,8 +72,11 @@ def restricted_search(S: Session, rows: tuple, cols: tuple, target: int, interva
         border = "continue" if preopen_vgap else "free"
     else:
         border = "restricted"
+    # prune kind 2: blocks from which no path can reach `target` are skipped
+    # (sound: every cell attaining target keeps its exact value)
     res = S.run([dict(rows=rows, cols=cols, border=border, clamp=False, track=track,
-                      band=interval)])[0]
+                      band=interval, prune=2 if S.target_prune else 0,
+                      prune_target=target)])[0]
     if res.best_i < 0 or res.best_score != target:
         found = res.best_score if res.best_i >= 0 else "none"
         raise StartNotFound(f"no cell attains the known score {target} (best found: {found}); "
