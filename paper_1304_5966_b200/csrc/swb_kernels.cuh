@@ -33,6 +33,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "swb_internal.h"
 
 namespace swb {
@@ -310,7 +312,9 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
 
   // One column of this lane's R rows.  GUARD: ramp blocks where some lanes
   // are outside [cb, ce).
-  auto step = [&](const int k, const int step_no, const bool guard, int (&Hin)[R], int (&Hout)[R]) {
+  auto step = [&](const int k, const int step_no, const bool guard, int (&Hin)[R], int (&Hout)[R],
+                  auto trk_tag) {
+    constexpr bool TRK = decltype(trk_tag)::value && (TRACK != kTrackNone);
     const int col = step_no - lane;
     const int4 rv = sm->ring[col & 63];
     int up_h = __shfl_up_sync(0xffffffffu, out_hm, 1);
@@ -338,7 +342,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
         d = Hin[r];
         Hout[r] = hm;
         hab = h2m;
-        if (TRACK != kTrackNone) {
+        if (TRK) {
           const int rank = (TRACK == kTrackMin) ? 31 - r : r;
           // padding rows (i >= n1, last strip only) need no guard: their
           // values are strictly below a real cell already seen (DESIGN.md
@@ -355,12 +359,12 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       }
       out_hm = Hout[R - 1];
       out_f = fv;
-      if (TRACK == kTrackMin) {
+      if (TRK && TRACK == kTrackMin) {
         if (cm > bkey) {
           bkey = cm;
           bj = col;
         }
-      } else if (TRACK == kTrackMax) {
+      } else if (TRK && TRACK == kTrackMax) {
         if (cm >= bkey) {
           bkey = cm;
           bj = col;
@@ -433,6 +437,10 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     // on a path that reaches the subproblem's end corner with the expected
     // score.  Skipped cells get the fill of engine.py:286-293.
     bool skip = false;
+    // Tracking is needed only where a cell could still reach the running best
+    // (a cell below it can never be the final answer): most blocks of a
+    // homologous pair run the untracked loop (no keys, no column max).
+    bool track_block = true;
     if (J.prune && steady) {
       int m = out_hm > diag ? out_hm : diag;
 #pragma unroll
@@ -447,6 +455,8 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       if (J.prune == 1) {
         const long long bound = (inm > 0 ? inm : 0) + ms * (long long)(rem_r < rem_c ? rem_r : rem_c);
         skip = bound < (long long)prune_seen;
+        // a path inside the 63-column-wide skewed block gains <= 63 * max_sub
+        track_block = (inm > 0 ? inm : 0) + 63LL * ms >= (long long)prune_seen;
       } else if (J.prune == 2) {
         const long long bound = inm + ms * (long long)(rem_r < rem_c ? rem_r : rem_c);
         skip = bound < (long long)J.prune_target;
@@ -486,17 +496,25 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       // (3) 32 steps.
       // two columns per iteration with ping-pong H registers: the old H of
       // a row (the next row's diagonal) survives without register moves
-      if (steady) {
+      using T1 = std::integral_constant<bool, true>;
+      using T0 = std::integral_constant<bool, false>;
+      if (steady && !track_block) {
 #pragma unroll 1
         for (int k = 0; k < 32; k += 2) {
-          step(k, s0 + k, false, H, H2);
-          step(k + 1, s0 + k + 1, false, H2, H);
+          step(k, s0 + k, false, H, H2, T0{});
+          step(k + 1, s0 + k + 1, false, H2, H, T0{});
+        }
+      } else if (steady) {
+#pragma unroll 1
+        for (int k = 0; k < 32; k += 2) {
+          step(k, s0 + k, false, H, H2, T1{});
+          step(k + 1, s0 + k + 1, false, H2, H, T1{});
         }
       } else {
 #pragma unroll 1
         for (int k = 0; k < 32; k += 2) {
-          step(k, s0 + k, true, H, H2);
-          step(k + 1, s0 + k + 1, true, H2, H);
+          step(k, s0 + k, true, H, H2, T1{});
+          step(k + 1, s0 + k + 1, true, H2, H, T1{});
         }
       }
       __syncwarp();
