@@ -131,14 +131,45 @@ int32_t swb_seq_upload(swb_ctx* ctx, const uint8_t* codes, int64_t n, int32_t* s
   if (n < 0 || (n > 0 && codes == nullptr) || seq_id == nullptr)
     return swb_fail(SWB_EINVAL, "swb_seq_upload: bad arguments");
   if (n >= (int64_t)1 << 31) return swb_fail(SWB_ERANGE, "sequence longer than 2^31-1");
-  for (int64_t x = 0; x < n; ++x)
-    if (codes[x] >= 7)
-      return swb_fail(SWB_EUNSUPPORTED, "residue code %d at offset %lld: alphabets of more than 7 symbols are not supported", (int)codes[x], (long long)x);
-  swb_seq sq;
+  {
+    uint8_t acc = 0;
+    for (int64_t x = 0; x < n; ++x) acc |= (uint8_t)(codes[x] >= 7);
+    if (acc) {
+      int64_t x = 0;
+      while (codes[x] < 7) ++x;
+      return swb_fail(SWB_EUNSUPPORTED,
+                      "residue code %d at offset %lld: alphabets of more than 7 symbols are not supported",
+                      (int)codes[x], (long long)x);
+    }
+  }
+  // reuse a released slot whose device buffers are large enough (released
+  // sequences keep their memory: no cudaMalloc/cudaFree per alignment call)
+  int slot = -1;
+  for (size_t k = 0; k < ctx->seqs.size(); ++k)
+    if (!ctx->seqs[k].live && ctx->seqs[k].cap >= n && (slot < 0 || ctx->seqs[k].cap < ctx->seqs[slot].cap))
+      slot = (int)k;
+  if (slot < 0) {
+    for (size_t k = 0; k < ctx->seqs.size(); ++k)
+      if (!ctx->seqs[k].live) {
+        slot = (int)k;
+        break;
+      }
+    if (slot < 0) {
+      ctx->seqs.push_back(swb_seq());
+      slot = (int)ctx->seqs.size() - 1;
+    }
+    swb_seq& sq = ctx->seqs[slot];
+    if (sq.fwd) cudaFree(sq.fwd);
+    if (sq.rev) cudaFree(sq.rev);
+    sq.fwd = sq.rev = nullptr;
+    sq.cap = 0;
+    const size_t bytes = n > 0 ? (size_t)n : 1;
+    SWB_CUDA(cudaMalloc(&sq.fwd, bytes));
+    SWB_CUDA(cudaMalloc(&sq.rev, bytes));
+    sq.cap = (int64_t)bytes;
+  }
+  swb_seq& sq = ctx->seqs[slot];
   sq.n = n;
-  size_t bytes = n > 0 ? (size_t)n : 1;
-  SWB_CUDA(cudaMalloc(&sq.fwd, bytes));
-  SWB_CUDA(cudaMalloc(&sq.rev, bytes));
   if (n > 0) {
     SWB_CUDA(cudaMemcpyAsync(sq.fwd, codes, (size_t)n, cudaMemcpyHostToDevice, ctx->stream));
     int blocks = (int)((n + 255) / 256);
@@ -149,15 +180,7 @@ int32_t swb_seq_upload(swb_ctx* ctx, const uint8_t* codes, int64_t n, int32_t* s
   }
   SWB_CUDA(cudaStreamSynchronize(ctx->stream));
   sq.live = true;
-  for (size_t k = 0; k < ctx->seqs.size(); ++k) {
-    if (!ctx->seqs[k].live) {
-      ctx->seqs[k] = sq;
-      *seq_id = (int32_t)k;
-      return SWB_OK;
-    }
-  }
-  ctx->seqs.push_back(sq);
-  *seq_id = (int32_t)(ctx->seqs.size() - 1);
+  *seq_id = (int32_t)slot;
   SWB_API_END();
 }
 
@@ -165,11 +188,7 @@ int32_t swb_seq_release(swb_ctx* ctx, int32_t seq_id) {
   SWB_API_BEGIN(ctx);
   if (seq_id < 0 || seq_id >= (int32_t)ctx->seqs.size() || !ctx->seqs[seq_id].live)
     return swb_fail(SWB_EINVAL, "bad sequence id %d", seq_id);
-  swb_seq& s = ctx->seqs[seq_id];
-  SWB_CUDA(cudaStreamSynchronize(ctx->stream));
-  cudaFree(s.fwd);
-  cudaFree(s.rev);
-  s = swb_seq();
+  ctx->seqs[seq_id].live = false;  // memory kept for reuse (freed with the context)
   SWB_API_END();
 }
 

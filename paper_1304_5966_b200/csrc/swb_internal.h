@@ -20,6 +20,7 @@ struct swb_seq {
   uint8_t* fwd = nullptr;  // device, n codes
   uint8_t* rev = nullptr;  // device, reversed copy
   int64_t n = 0;
+  int64_t cap = 0;  // allocated bytes of fwd / rev
   bool live = false;
 };
 
