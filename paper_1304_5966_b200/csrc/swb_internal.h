@@ -46,6 +46,8 @@ struct swb_ctx {
   int claim_mode = 0;
   bool trace = false;
   int mm_prune = 1;
+  int x2_enabled = 1;
+  int x2_R = 0;  // force the packed kernel's rows per lane (diagnostics)
   std::vector<unsigned long long> dbg_times;
   // scratch
   swb_buf jobs, rowbuf, progress, results, finals, misc, host_pinned, flush;

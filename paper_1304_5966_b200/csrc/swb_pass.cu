@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "swb_kernels.cuh"
+#include "swb_x2.cuh"
 #include "swb_passes.h"
 
 using namespace swb;
@@ -101,9 +102,8 @@ int kernel_occupancy(int* per_sm) {
                                                             128, 0);
 }
 
-template <int R, bool LOCAL, int TRACK>
-int launch_kernel(swb_ctx* ctx, const PassParams& Pin, long long items, int ctas_per_sm) {
-  auto kern = pass_kernel<R, LOCAL, TRACK>;
+template <typename K>
+int launch_any(swb_ctx* ctx, K kern, const PassParams& Pin, long long items, int ctas_per_sm) {
   PassParams P = Pin;
   int per_sm = 0;
   SWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, 0));
@@ -136,6 +136,33 @@ int launch_kernel(swb_ctx* ctx, const PassParams& Pin, long long items, int ctas
   ctx->launches++;
   SWB_CUDA(cudaGetLastError());
   return SWB_OK;
+}
+
+template <int R, bool LOCAL, int TRACK>
+int launch_kernel(swb_ctx* ctx, const PassParams& Pin, long long items, int ctas_per_sm) {
+  return launch_any(ctx, pass_kernel<R, LOCAL, TRACK>, Pin, items, ctas_per_sm);
+}
+
+// packed 16x2 phase-1 kernel (swb_x2.cuh): R packed rows per lane, 64R rows per item
+constexpr int kX2R[] = {8, 12, 16};
+
+template <int R>
+int dispatch_x2_R(swb_ctx* ctx, const PassParams* P, long long items, int ctas_per_sm,
+                  int* occ_out) {
+  if (occ_out)
+    return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ_out, pass_kernel_x2<R>, 128, 0);
+  return launch_any(ctx, pass_kernel_x2<R>, *P, items, ctas_per_sm);
+}
+
+int dispatch_x2(swb_ctx* ctx, int R, const PassParams* P, long long items, int ctas_per_sm,
+                int* occ_out) {
+  switch (R) {
+    case 8: return dispatch_x2_R<8>(ctx, P, items, ctas_per_sm, occ_out);
+    case 12: return dispatch_x2_R<12>(ctx, P, items, ctas_per_sm, occ_out);
+    case 16: return dispatch_x2_R<16>(ctx, P, items, ctas_per_sm, occ_out);
+    default: break;
+  }
+  return swb_fail(SWB_EINVAL, "packed rows_per_lane %d not instantiated", R);
 }
 
 template <int R>
@@ -193,23 +220,31 @@ struct Shape {
   int ctas_per_sm = 0;
 };
 
-Shape choose_shape(swb_ctx* ctx, const std::vector<PassReq*>& jobs, bool local, int track) {
-  const int* cand = local ? kLocalR : kOtherR;
-  const int ncand = local ? (int)(sizeof(kLocalR) / sizeof(int)) : (int)(sizeof(kOtherR) / sizeof(int));
+Shape choose_shape(swb_ctx* ctx, const std::vector<PassReq*>& jobs, bool local, int track,
+                   bool x2) {
+  const int* cand = x2 ? kX2R : (local ? kLocalR : kOtherR);
+  const int ncand = x2 ? (int)(sizeof(kX2R) / sizeof(int))
+                       : (local ? (int)(sizeof(kLocalR) / sizeof(int))
+                                : (int)(sizeof(kOtherR) / sizeof(int)));
+  const int rows_mul = x2 ? 64 : 32;
   const int smsp = ctx->sms * 4;
   Shape best;
   double best_t = 1e300;
   for (int q = 0; q < ncand; ++q) {
     const int R = cand[q];
     int occ = 0;
-    if (dispatch(ctx, R, nullptr, 0, local, track, 0, &occ) != cudaSuccess || occ < 1) continue;
+    const int rc = x2 ? dispatch_x2(ctx, R, nullptr, 0, 0, &occ)
+                      : dispatch(ctx, R, nullptr, 0, local, track, 0, &occ);
+    if (rc != cudaSuccess || occ < 1) continue;
+    const long long rows_item = (long long)rows_mul * R;
     long long strips = 0, chain = 0;
     for (const PassReq* r : jobs) {
-      const long long sj = (r->n1 + 32LL * R - 1) / (32LL * R);
+      const long long sj = (r->n1 + rows_item - 1) / rows_item;
       strips += sj;
-      chain = std::max(chain, (long long)r->n2 + 64LL * sj);
+      chain = std::max(chain, (long long)r->n2 + (x2 ? 128LL : 64LL) * sj);
     }
-    const double alu = 2.0 * (5.7 * R + 10.0);
+    // integer-ALU cycles per warp-step: 5.7 per row (x2: 2.7 per packed row pair)
+    const double alu = x2 ? 2.0 * (2.9 * R + 16.0) : 2.0 * (5.7 * R + 10.0);
     const double lat = 1.7 * alu;
     const long long w_need = (strips + smsp - 1) / smsp;
     const int w = (int)std::min<long long>(w_need, occ);
@@ -218,7 +253,7 @@ Shape choose_shape(swb_ctx* ctx, const std::vector<PassReq*>& jobs, bool local, 
     // total work bound vs chain bound
     double work = 0.0;
     for (const PassReq* r : jobs)
-      work += (double)((r->n1 + 32LL * R - 1) / (32LL * R)) * (double)(r->n2 + 64) * alu;
+      work += (double)((r->n1 + rows_item - 1) / rows_item) * (double)(r->n2 + 64) * alu;
     const double t = std::max((double)rounds * (double)chain * step, work / smsp);
     if (t < best_t * 0.999) {
       best_t = t;
@@ -261,15 +296,28 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
       return swb_fail(SWB_ERANGE, "tracked pass %d x %d exceeds the 26-bit score key range",
                       r.n1, r.n2);
   }
-  // one launch per (recurrence, tracking) class; rows-per-lane per class
-  auto cls = [&](int q) { return (reqs[q].local ? 10 : 0) + reqs[q].track; };
+  // packed 16x2 fast path eligibility (swb_x2.cuh header)
+  bool x2_scheme = sc.k <= 4 && ctx->x2_enabled;
+  for (int b = 0; b < sc.k && x2_scheme; ++b)
+    for (int a = 0; a < sc.k; ++a) {
+      const int v = (int)(int8_t)((sc.tlo[b] >> (8 * a)) & 0xff);
+      if (v < 0 || v > 127) x2_scheme = false;
+    }
+  for (PassReq& r : reqs)
+    r.x2 = x2_scheme && r.local && r.track == kTrackMin && !r.has_band && !r.want_final &&
+           !r.ext_in && !r.ext_out && r.row_offset == 0 && r.prune <= 1 && r.force_R == 0;
+  // one launch per (recurrence, tracking, kernel) class; rows-per-lane per class
+  auto cls = [&](int q) {
+    return (reqs[q].x2 ? 100 : 0) + (reqs[q].local ? 10 : 0) + reqs[q].track;
+  };
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cls(a) < cls(b); });
   std::vector<int> cls_ctas(reqs.size(), 0);
   for (size_t a = 0; a < order.size();) {
     size_t b = a;
     std::vector<PassReq*> js;
     while (b < order.size() && cls(order[b]) == cls(order[a])) js.push_back(&reqs[order[b++]]);
-    Shape sh = choose_shape(ctx, js, js[0]->local, js[0]->track);
+    Shape sh = choose_shape(ctx, js, js[0]->local, js[0]->track, js[0]->x2);
+    if (js[0]->x2 && ctx->x2_R) sh.R = ctx->x2_R;
     for (PassReq* r : js) {
       r->R = r->force_R ? r->force_R : sh.R;
       cls_ctas[r - &reqs[0]] = sh.ctas_per_sm;
@@ -296,7 +344,8 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     long long total_strips = 0, total_cols = 0, final_cols = 0;
     for (size_t t = g0; t < g1; ++t) {
       PassReq& r = reqs[order[t]];
-      r.nstrips = (int)((r.n1 + 32LL * R - 1) / (32LL * R));
+      const long long rows_item = (r.x2 ? 64LL : 32LL) * R;
+      r.nstrips = (int)((r.n1 + rows_item - 1) / rows_item);
       total_strips += r.nstrips;
       total_cols += r.n2;
       if (r.want_final && r.fin_h_dev == nullptr) final_cols += r.n2;
@@ -415,7 +464,8 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     SWB_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
     int rc;
     int ctas = ctx->max_ctas_per_sm ? ctx->max_ctas_per_sm : cls_ctas[order[g0]];
-    rc = dispatch(ctx, R, &P, item, head.local, head.track, ctas, nullptr);
+    rc = head.x2 ? dispatch_x2(ctx, R, &P, item, ctas, nullptr)
+                 : dispatch(ctx, R, &P, item, head.local, head.track, ctas, nullptr);
     if (rc) return rc;
     SWB_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
     SWB_CUDA(cudaMemcpyAsync(h_res, d_res, sizeof(int4) * total_strips, cudaMemcpyDeviceToHost,
@@ -521,6 +571,14 @@ extern "C" int32_t swb_set_option(swb_ctx* ctx, const char* name, int64_t value)
   if (!ctx || !name) return swb_fail(SWB_EINVAL, "bad arguments");
   if (!strcmp(name, "max_ctas_per_sm")) {
     ctx->max_ctas_per_sm = (int)value;
+    return SWB_OK;
+  }
+  if (!strcmp(name, "x2_R")) {
+    ctx->x2_R = (int)value;
+    return SWB_OK;
+  }
+  if (!strcmp(name, "x2")) {
+    ctx->x2_enabled = (int)value;
     return SWB_OK;
   }
   if (!strcmp(name, "mm_prune")) {

@@ -34,6 +34,7 @@ struct PassReq {
   int32_t* ext_out_prog = nullptr;
   // filled by swb_run_passes
   int R = 0;
+  bool x2 = false;  // packed 16x2 phase-1 kernel
   int nstrips = 0;
   long long res_offset = 0;
   long long best_score = 0, best_i = -1, best_j = -1;

@@ -1,0 +1,459 @@
+// Packed 16x2 score pass (phase 1 fast path).
+//
+// One warp runs a 64-lane virtual pipeline: the low 16 bits of every register
+// hold strip A (rows [R0, R0 + 32R)), the high 16 bits strip B (the next 32R
+// rows).  Lane l processes column s - l of A and column s - l - 32 of B at step
+// s, so B's lane 0 consumes A's lane 31 output of the previous step (one extra
+// shuffle) and B's bottom row is the item's output to the next warp.  Every DP
+// instruction is a DPX S16x2 op or a carry-free 32-bit IMAD on two 16-bit
+// fields, i.e. two cells per instruction:
+//
+//   s   = PRMT(T[colA], T[colB], sel_r)           two zero-extended bytes (sub + go + ge)
+//   ds  = IMAD(hm_diag, 1, s)                     packed add, no carry (fields in [0, 32767])
+//   h2  = VIMNMX3.S16x2(ds, E, FLOOR)             max(diag + sub, E, floor)
+//   F   = VIADDMNMX.S16x2(F, -ge, h2m_above)
+//   h2m = IMAD(h2, 1, -(go+ge) packed)            packed subtract, no borrow (h2 >= FLOOR)
+//   hm  = VIADDMNMX.S16x2(F, -(go+ge), h2m)
+//   E'  = VIADDMNMX.S16x2(E, -ge, hm)
+//
+// Values are stored relative to a warp-wide base: rel = abs - base + 1024.
+// FLOOR (rel 1024) is abs max(0, base): with base = 0 it is the local-alignment
+// clamp at 0 exactly; with base > 0 it only raises values that lie more than
+// 26000 below the warp's maximum, which no true value in the warp's window can
+// (adjacent DP cells differ by at most max_sub + go + ge and the window is
+// 2048 rows x 95 columns), so every value stays a lower bound of the truth and
+// every value on an optimal path stays exact.  The base is
+// re-chosen every 32 steps from the warp maximum and the incoming top row.
+//
+// Scope: local passes, TRACK_MIN, no band, no final rows, alphabets of <= 4
+// codes with 0 <= sub + go + ge <= 127.  Everything else uses run_strip.
+#pragma once
+
+#include "swb_kernels.cuh"
+
+namespace swb {
+
+constexpr int kX2Off = 1024;     // rel value of the floor
+constexpr int kX2Span = 26000;   // max - base kept below this
+
+struct WarpSmemX2 {
+  int4 ring[128];  // per column c: (top hm abs, top F abs, profile word, -) at [c & 127]
+  int2 out[32];
+};
+
+__device__ __forceinline__ uint32_t vimax3_2(uint32_t a, uint32_t b, uint32_t c) {
+  return (uint32_t)__vimax3_s16x2((int)a, (int)b, (int)c);
+}
+__device__ __forceinline__ uint32_t viaddmax_2(uint32_t a, uint32_t b, uint32_t c) {
+  return (uint32_t)__viaddmax_s16x2((int)a, (int)b, (int)c);
+}
+__device__ __forceinline__ uint32_t pack2(int lo, int hi) {
+  return ((uint32_t)lo & 0xffffu) | ((uint32_t)hi << 16);
+}
+__device__ __forceinline__ int lo16(uint32_t x) { return (int)(short)(x & 0xffffu); }
+__device__ __forceinline__ int hi16(uint32_t x) { return (int)x >> 16; }
+__device__ __forceinline__ int clamp_rel(long long v) {
+  return v < 0 ? 0 : (v > 32767 ? 32767 : (int)v);
+}
+
+template <int R, bool TRK_ANY>
+__device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& Jg, int s,
+                                          WarpSmemX2* sm, const uint32_t* __restrict__ tw_s) {
+  const JobDev J = Jg;
+  const int lane = threadIdx.x & 31;
+  const int goe = P.goe, ge = P.ge;
+  const int n1 = J.n1, n2 = J.n2;
+  const int R0 = s * 64 * R;
+  const int rowA = R0 + lane * R;
+  const int rowB = R0 + 32 * R + lane * R;
+  const int2* __restrict__ inbuf = J.buf[(s + 1) & 1];
+  int2* __restrict__ outbuf = J.buf[s & 1];
+  int32_t* my_progress = J.progress + s;
+  const int32_t* up_progress = s > 0 ? J.progress + (s - 1) : nullptr;
+
+  // selectors: byte0 <- T[colA] byte a, byte2 <- T[colB] byte b, bytes 1 and 3
+  // replicate the (zero) sign of a profile byte; padding rows select zeros.
+  uint32_t sel[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int ia = rowA + r, ib = rowB + r;
+    const uint32_t a = (ia < n1) ? (uint32_t)J.rows[(long long)ia * J.rstep] : 8u;
+    const uint32_t b = (ib < n1) ? 4u + (uint32_t)J.rows[(long long)ib * J.rstep] : 8u;
+    sel[r] = a | ((a | 8u) << 4) | (b << 8) | ((b | 8u) << 12);
+  }
+
+  const uint32_t FLOOR2 = pack2(kX2Off, kX2Off);
+  const uint32_t ZERO2 = 0u;
+  const uint32_t NGE2 = pack2(-ge, -ge);
+  const uint32_t NGOE2 = pack2(-goe, -goe);
+  const int NGOE32 = -(goe * 65536 + goe);  // carry-free packed subtract of goe
+  int base = 0;
+  // local left border: H = 0 -> hm = -goe; E = max(NEG - ge, hm) = hm
+  const uint32_t hm0 = pack2(kX2Off - goe, kX2Off - goe);
+  uint32_t H[R], H2[R], E[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    H[r] = hm0;
+    H2[r] = hm0;
+    E[r] = hm0;
+  }
+  uint32_t diag = hm0;
+  uint32_t out_hm = hm0, out_f = 0u;
+
+  int bkeyA = (-goe) * 32 + 31, bkeyB = (-goe) * 32 + 31;
+  int bjA = -1, bjB = -1;
+  const int k32 = P.key_mul;
+  int known_prog = 0, prune_seen = 0;
+  int code_next = (lane < n2) ? (int)J.cols[(long long)lane * J.cstep] : 0;
+  long long pruned_blocks = 0, exec_blocks = 0, wait_cycles = 0;
+  const long long t_strip0 = clock64();
+  unsigned long long g0, gw = 0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+  const int s_end = n2 + 63;
+  // Every ring slot an inactive half may read must hold a valid profile word:
+  // a stale byte >= 128 would be sign-replicated by PRMT and its carry in the
+  // packed IMAD add would corrupt the other (active) half.
+#pragma unroll
+  for (int q = lane; q < 128; q += 32) sm->ring[q] = make_int4(-goe, SWB_NEG32, 0, 0);
+  __syncwarp();
+
+  auto step = [&](const int k, const int st, const bool guard, uint32_t (&Hin)[R],
+                  uint32_t (&Hout)[R], auto trk_tag) {
+    constexpr bool TRK = decltype(trk_tag)::value && TRK_ANY;
+    const int colA = st - lane, colB = colA - 32;
+    const int4 ra = sm->ring[colA & 127];
+    const int4 rb = sm->ring[colB & 127];
+    uint32_t up_h = __shfl_up_sync(0xffffffffu, out_hm, 1);
+    uint32_t up_f = __shfl_up_sync(0xffffffffu, out_f, 1);
+    const uint32_t x_h = __shfl_sync(0xffffffffu, out_hm, 31);
+    const uint32_t x_f = __shfl_sync(0xffffffffu, out_f, 31);
+    if (lane == 0) {
+      const long long off = (long long)kX2Off - base;
+      up_h = pack2(clamp_rel((long long)ra.x + off), lo16(x_h));
+      up_f = pack2(clamp_rel((long long)ra.y + off), lo16(x_f));
+    }
+    const bool actA = colA >= 0 && colA < n2;
+    const bool actB = colB >= 0 && colB < n2;
+    if (guard && !actA && !actB) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) Hout[r] = Hin[r];
+      return;
+    }
+    const uint32_t keep = guard ? ((actA ? 0u : 0xffffu) | (actB ? 0u : 0xffff0000u)) : 0u;
+    const uint32_t tl = (uint32_t)ra.z, th = (uint32_t)rb.z;
+    uint32_t d = diag;
+    diag = guard ? ((up_h & ~keep) | (diag & keep)) : up_h;
+    uint32_t fv = up_f;
+    uint32_t hab = up_h;
+    int cmA = INT32_MIN, cmB = INT32_MIN, kpA = INT32_MIN, kpB = INT32_MIN;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint32_t sv = prmt(tl, th, sel[r]);
+      const uint32_t ds = (uint32_t)imad((int)d, 1, (int)sv);
+      const uint32_t h2 = vimax3_2(ds, E[r], FLOOR2);
+      fv = viaddmax_2(fv, NGE2, hab);
+      const uint32_t h2m = (uint32_t)imad((int)h2, 1, NGOE32);
+      const uint32_t hm = viaddmax_2(fv, NGOE2, h2m);
+      const uint32_t en = viaddmax_2(E[r], NGE2, hm);
+      E[r] = guard ? ((en & ~keep) | (E[r] & keep)) : en;
+      d = Hin[r];
+      Hout[r] = guard ? ((hm & ~keep) | (Hin[r] & keep)) : hm;
+      hab = h2m;
+      if (TRK) {
+        const int ka = imad(lo16(hm), k32, 31 - r);
+        const int kb = imad(hi16(hm), k32, 31 - r);
+        if (r & 1) {
+          cmA = __vimax3_s32(cmA, kpA, ka);
+          cmB = __vimax3_s32(cmB, kpB, kb);
+        } else if (r == R - 1) {
+          cmA = cmA > ka ? cmA : ka;
+          cmB = cmB > kb ? cmB : kb;
+        }
+        kpA = ka;
+        kpB = kb;
+      }
+    }
+    out_hm = Hout[R - 1];
+    out_f = fv;
+    if (TRK) {
+      const int kb_off = (base - kX2Off) * 32;
+      if (actA && cmA + kb_off > bkeyA) {
+        bkeyA = cmA + kb_off;
+        bjA = colA;
+      }
+      if (actB && cmB + kb_off > bkeyB) {
+        bkeyB = cmB + kb_off;
+        bjB = colB;
+      }
+    }
+    if (lane == 31 && actB) {
+      const int off = base - kX2Off;
+      sm->out[k] = make_int2(hi16(out_hm) + off, hi16(out_f) + off);
+    }
+  };
+
+  for (int s0 = 0; s0 < s_end; s0 += 32) {
+    // (1) stage the producer's bottom row and profile words for [s0, s0+32)
+    {
+      const int c = s0 + lane;
+      const int code = code_next;
+      const int pb_now = J.prune == 1 ? ld_relaxed(J.prune_best) : 0;
+      {
+        const int cn = c + 32;
+        code_next = (cn < n2) ? (int)J.cols[(long long)cn * J.cstep] : 0;
+      }
+      if (s > 0 && s0 < n2) {
+        const int need = (s0 + 32 < n2) ? s0 + 32 : n2;
+        if (known_prog < need) {
+          if (ld_relaxed(up_progress) < need) {
+            const long long tw = clock64();
+            unsigned long long a0, a1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a0));
+            wait_progress(up_progress, need);
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a1));
+            gw += a1 - a0;
+            wait_cycles += clock64() - tw;
+          }
+          known_prog = ld_acquire(up_progress);
+        }
+      }
+      if (c < n2) {
+        int th = -goe, tf = SWB_NEG32;  // local top border: H = 0, F = -inf
+        if (s > 0) {
+          const int2 v = __ldcg(inbuf + c);
+          th = v.x;
+          tf = v.y;
+        }
+        sm->ring[c & 127] = make_int4(th, tf, (int)tw_s[code], 0);
+      } else {
+        sm->ring[c & 127] = make_int4(-goe, SWB_NEG32, 0, 0);
+      }
+      prune_seen = pb_now;
+      __syncwarp();
+    }
+
+    // (1b) re-base: warp maximum over the state and the staged top row
+    int mrel = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      mrel = __vimax3_s32(mrel, lo16(H[r]), hi16(H[r]));
+    }
+    mrel = __vimax3_s32(mrel, lo16(out_hm), hi16(out_hm));
+    long long mabs = (long long)mrel + base - kX2Off;  // hm (H - go - ge), absolute
+    {
+      const int c = s0 + lane;
+      if (c < n2) {
+        const int tv = sm->ring[c & 127].x;
+        if ((long long)tv > mabs) mabs = tv;
+      }
+    }
+    const int mabs_w = __reduce_max_sync(0xffffffffu, (int)(mabs > INT32_MAX ? INT32_MAX : mabs));
+    {
+      long long nb = (long long)mabs_w + goe - kX2Span;
+      if (nb < 0) nb = 0;
+      if (nb != base) {
+        const int delta = (int)(nb - base);
+        const int dd = delta > 32767 ? 32767 : (delta < -32767 ? -32767 : delta);
+        // shift by -delta per field, clamping at rel 0 (a lower bound, see header)
+        uint32_t sh = pack2(-dd, -dd);
+        int rem = delta - dd;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          H[r] = viaddmax_2(H[r], sh, ZERO2);
+          E[r] = viaddmax_2(E[r], sh, ZERO2);
+        }
+        diag = viaddmax_2(diag, sh, ZERO2);
+        out_hm = viaddmax_2(out_hm, sh, ZERO2);
+        out_f = viaddmax_2(out_f, sh, ZERO2);
+        while (rem != 0) {  // very large jumps (after long pruned runs)
+          const int d2 = rem > 32767 ? 32767 : (rem < -32767 ? -32767 : rem);
+          sh = pack2(-d2, -d2);
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            H[r] = viaddmax_2(H[r], sh, ZERO2);
+            E[r] = viaddmax_2(E[r], sh, ZERO2);
+          }
+          diag = viaddmax_2(diag, sh, ZERO2);
+          out_hm = viaddmax_2(out_hm, sh, ZERO2);
+          out_f = viaddmax_2(out_f, sh, ZERO2);
+          rem -= d2;
+        }
+        base = (int)nb;
+      }
+    }
+    const bool steady = (s0 >= 63) && (s0 + 32 <= n2);
+
+    // (2) pruning / tracking decision on the 95-column skewed block
+    bool skip = false, track_block = true;
+    if (J.prune == 1 && steady) {
+      const long long inm = (long long)mabs_w + goe;
+      const long long ms = P.max_sub;
+      const int rem_r = n1 - R0;
+      const int rem_c = n2 - (s0 - 63);
+      const long long bound = (inm > 0 ? inm : 0) + ms * (long long)(rem_r < rem_c ? rem_r : rem_c);
+      skip = bound < (long long)prune_seen;
+      track_block = (inm > 0 ? inm : 0) + 95LL * ms >= (long long)prune_seen;
+    }
+
+    if (skip) {
+      ++pruned_blocks;
+      // fill: H = 0 (hm = -goe), E/F = -inf (clamped at the floor)
+      const int hf = clamp_rel((long long)-goe - base + kX2Off);
+      const uint32_t fill = pack2(hf, hf);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        H[r] = fill;
+        E[r] = fill;
+      }
+      // lane 0's next diagonal is the real top input of the block's last column
+      diag = fill;
+      if (lane == 0) {
+        const int t = sm->ring[(s0 + 31) & 127].x;
+        diag = pack2(clamp_rel((long long)t - base + kX2Off), hf);
+      }
+      out_hm = fill;
+      out_f = 0u;
+      sm->out[lane] = make_int2(-goe, SWB_NEG32);
+      __syncwarp();
+    } else {
+      ++exec_blocks;
+      using T1 = std::integral_constant<bool, true>;
+      using T0 = std::integral_constant<bool, false>;
+      if (steady && !track_block) {
+#pragma unroll 1
+        for (int k = 0; k < 32; k += 2) {
+          step(k, s0 + k, false, H, H2, T0{});
+          step(k + 1, s0 + k + 1, false, H2, H, T0{});
+        }
+      } else if (steady) {
+#pragma unroll 1
+        for (int k = 0; k < 32; k += 2) {
+          step(k, s0 + k, false, H, H2, T1{});
+          step(k + 1, s0 + k + 1, false, H2, H, T1{});
+        }
+      } else {
+#pragma unroll 1
+        for (int k = 0; k < 32; k += 2) {
+          step(k, s0 + k, true, H, H2, T1{});
+          step(k + 1, s0 + k + 1, true, H2, H, T1{});
+        }
+      }
+      __syncwarp();
+    }
+
+    // (4) flush B's bottom row for columns [s0 - 63, s0 - 31) and publish
+    {
+      const int c = s0 - 63 + lane;
+      if (c >= 0 && c < n2) __stcg(outbuf + c, sm->out[lane]);
+      __syncwarp();
+      if (lane == 0) {
+        int pub = s0 - 31;
+        if (pub > n2) pub = n2;
+        if (pub > 0) st_release(my_progress, pub);
+      }
+    }
+
+    // (5) running best for pruning
+    if (J.prune == 1) {
+      const int bm = __reduce_max_sync(0xffffffffu, (bkeyA > bkeyB ? bkeyA : bkeyB) >> 5);
+      if (lane == 0 && bm > -goe) atomicMax(J.prune_best, bm + goe);
+    }
+  }
+  if (lane == 0) st_release(my_progress, n2);
+
+  // item result: best of both halves, then warp reduction (smallest (i, j) on ties)
+  int b = bkeyA >> 5, ii = -1, jj = -1;
+  if (bjA >= 0) {
+    ii = rowA + (31 - (bkeyA & 31));
+    jj = bjA;
+  }
+  if (bjB >= 0) {
+    const int bb = bkeyB >> 5;
+    const int ib = rowB + (31 - (bkeyB & 31));
+    if (ii < 0 || bb > b || (bb == b && (ib < ii || (ib == ii && bjB < jj)))) {
+      b = bb;
+      ii = ib;
+      jj = bjB;
+    }
+  }
+  if (ii >= n1) ii = jj = -1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int ob = __shfl_down_sync(0xffffffffu, b, o);
+    const int oi = __shfl_down_sync(0xffffffffu, ii, o);
+    const int oj = __shfl_down_sync(0xffffffffu, jj, o);
+    bool take;
+    if (oi < 0) take = false;
+    else if (ii < 0) take = true;
+    else take = ob > b || (ob == b && (oi < ii || (oi == ii && oj < jj)));
+    if (take) {
+      b = ob;
+      ii = oi;
+      jj = oj;
+    }
+  }
+  if (lane == 0) {
+    J.strip_res[s] = make_int4(b, ii, jj, ii >= 0 ? 1 : 0);
+    int rows_here = n1 - R0;
+    if (rows_here > 64 * R) rows_here = 64 * R;
+    const long long cells = (long long)n2 * rows_here - pruned_blocks * 32LL * rows_here;
+    atomicAdd(&J.counters[0], (unsigned long long)(cells > 0 ? cells : 0));
+    atomicAdd(&J.counters[1], (unsigned long long)exec_blocks);
+    atomicAdd(&J.counters[2], (unsigned long long)pruned_blocks);
+    atomicAdd(&J.counters[3], (unsigned long long)wait_cycles);
+    atomicAdd(&J.counters[4], (unsigned long long)(clock64() - t_strip0));
+    unsigned long long g1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+    J.strip_times[3 * s + 0] = g0;
+    J.strip_times[3 * s + 1] = g1;
+    J.strip_times[3 * s + 2] = gw;
+  }
+}
+
+template <int R>
+__global__ void __launch_bounds__(256, 1) pass_kernel_x2(const PassParams P) {
+  __shared__ WarpSmemX2 wsm[8];
+  __shared__ uint32_t tw_s[8];
+  __shared__ long long base_s;
+  if (threadIdx.x < 8) tw_s[threadIdx.x] = P.tlo[threadIdx.x];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  WarpSmemX2* sm = &wsm[warp];
+  auto run = [&](long long item) {
+    int lo = 0, hi = P.njobs - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (P.jobs[mid].item_base <= item) lo = mid;
+      else hi = mid - 1;
+    }
+    run_strip_x2<R, true>(P, P.jobs[lo], (int)(item - P.jobs[lo].item_base), sm, tw_s);
+  };
+  if (P.group > 0) {
+    const int w = (int)(blockDim.x >> 7);
+    for (;;) {
+      if (threadIdx.x == 0) base_s = (long long)atomicAdd(P.claim, (unsigned long long)P.group);
+      __syncthreads();
+      const long long base = base_s;
+      __syncthreads();
+      if (base >= P.total_items) break;
+      long long item = base + (warp & 3) * w + (warp >> 2);
+      if (P.mirror) {
+        const long long p = base / 2 + (warp & 3);
+        const long long q = P.total_items - 1 - p;
+        item = (warp >> 2) == 0 ? (p <= q ? p : P.total_items) : (p < q ? q : P.total_items);
+      }
+      if (item < P.total_items) run(item);
+    }
+    return;
+  }
+  for (;;) {
+    long long item = 0;
+    if (lane == 0) item = (long long)atomicAdd(P.claim, 1ULL);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= P.total_items) break;
+    run(item);
+  }
+}
+
+}  // namespace swb
