@@ -215,9 +215,14 @@ typedef struct {
 } swb_int_peak;
 int32_t swb_measure_int_peak(swb_ctx* ctx, swb_int_peak* out);
 
-/* Tuning knobs: "max_ctas_per_sm" (0 = occupancy limit) and "rows_per_lane"
- * (0 = automatic, else 2, 8 or 32 rows of seq1 per lane). */
+/* Tuning knobs: "max_ctas_per_sm" (0 = occupancy limit), "rows_per_lane"
+ * (0 = automatic, else an instantiated rows-per-lane), "x2" (1 = allow the
+ * packed 16x2 score-pass kernel), "x2_R" (its rows per lane, 0 = automatic),
+ * "mm_prune" (corner-target pruning in Myers-Miller halves), "claim_mode"
+ * (0 auto, 1 CTA claiming, 2 warp claiming), "proto", "reset_debug". */
 int32_t swb_set_option(swb_ctx* ctx, const char* name, int64_t value);
+/* Current value of a tuning option (-1 for an unknown name). */
+int64_t swb_get_option(swb_ctx* ctx, const char* name);
 
 /* Diagnostics: out[0] = cycles warps spent waiting on the strip above,
  * out[1] = total strip cycles, summed over all passes since "reset_debug". */

@@ -70,7 +70,7 @@ class IntPeak(ctypes.Structure):
 EXPORTS = (
     "swb_ctx_create", "swb_ctx_destroy", "swb_last_error", "swb_version", "swb_seq_upload",
     "swb_seq_release", "swb_pass", "swb_crossings", "swb_leaves", "swb_measure_int_peak",
-    "swb_last_kernel_ms", "swb_launch_count", "swb_set_option", "swb_debug_stats",
+    "swb_last_kernel_ms", "swb_launch_count", "swb_set_option", "swb_get_option", "swb_debug_stats",
     "swb_debug_times", "swb_timer_start", "swb_timer_stop", "swb_flush_l2",
     "swb_boundary_alloc", "swb_boundary_reset", "swb_boundary_free", "swb_ipc_export",
     "swb_ipc_import", "swb_ipc_close",
@@ -118,6 +118,8 @@ def load() -> ctypes.CDLL:
         lib.swb_launch_count.restype = c_i64
         lib.swb_set_option.argtypes = [c_p, ctypes.c_char_p, c_i64]
         lib.swb_set_option.restype = c_i32
+        lib.swb_get_option.argtypes = [c_p, ctypes.c_char_p]
+        lib.swb_get_option.restype = c_i64
         lib.swb_debug_stats.argtypes = [c_p, c_p, c_i32]
         lib.swb_debug_stats.restype = c_i32
         lib.swb_debug_times.argtypes = [c_p, c_p, c_i32]

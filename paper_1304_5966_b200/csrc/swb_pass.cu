@@ -567,6 +567,18 @@ static inline long long widen(int32_t v) {
   return v;
 }
 
+extern "C" int64_t swb_get_option(swb_ctx* ctx, const char* name) {
+  if (!ctx || !name) return -1;
+  if (!strcmp(name, "max_ctas_per_sm")) return ctx->max_ctas_per_sm;
+  if (!strcmp(name, "x2_R")) return ctx->x2_R;
+  if (!strcmp(name, "x2")) return ctx->x2_enabled;
+  if (!strcmp(name, "mm_prune")) return ctx->mm_prune;
+  if (!strcmp(name, "claim_mode")) return ctx->claim_mode;
+  if (!strcmp(name, "proto")) return ctx->proto;
+  if (!strcmp(name, "rows_per_lane")) return ctx->force_R;
+  return -1;
+}
+
 extern "C" int32_t swb_set_option(swb_ctx* ctx, const char* name, int64_t value) {
   if (!ctx || !name) return swb_fail(SWB_EINVAL, "bad arguments");
   if (!strcmp(name, "max_ctas_per_sm")) {

@@ -127,6 +127,9 @@ class DeviceContext:
     def set_option(self, name: str, value: int) -> None:
         _lib.check(self.lib.swb_set_option(self.ptr, name.encode(), int(value)), "swb_set_option")
 
+    def get_option(self, name: str) -> int:
+        return int(self.lib.swb_get_option(self.ptr, name.encode()))
+
     def timer_start(self) -> None:
         _lib.check(self.lib.swb_timer_start(self.ptr), "swb_timer_start")
 

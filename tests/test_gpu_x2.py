@@ -18,12 +18,13 @@ def _both(a, b, scheme, prune=True):
     s1 = Sequence.from_codes("a", a, scheme.alphabet)
     s2 = Sequence.from_codes("b", b, scheme.alphabet)
     out = []
+    default = ctx.get_option("x2")
     for flag in (1, 0):
         ctx.set_option("x2", flag)
         rep = {}
         r = swb.score_only(s1, s2, scheme, AlignConfig(prune=prune), report=rep)
         out.append((r.score, tuple(r.end)))
-    ctx.set_option("x2", 1)
+    ctx.set_option("x2", default)
     return out
 
 

@@ -17,6 +17,9 @@ b = random_codes(rng, n) if unrel else mutate_codes(rng, a, 0.10)
 sc = dna_scheme()
 s1 = swb.Sequence.from_codes("a", a, sc.alphabet)
 s2 = swb.Sequence.from_codes("b", b, sc.alphabet)
+import os
+if "X2" in os.environ:
+    swb.get_context(0).set_option("x2", int(os.environ["X2"]))
 rep = {}
 r = swb.score_only(s1, s2, sc, report=rep)
 print(r, rep)

@@ -21,7 +21,7 @@ for hom in (True, False):
             best = 1e9
             for _ in range(3):
                 r = swb.score_only(s1, s2, sc, swb.AlignConfig(prune=prune))
-                best = min(best, ctx.last_kernel_ms())
+                best = min(best, ctx.last_kernel_ms)
             print(f"hom={hom} prune={prune} x2={flag} R={R}: {best:.1f} ms "
                   f"{a.size * b.size / best / 1e6:.0f} GCUPS  score={r.score}", flush=True)
 ctx.set_option("x2", 1); ctx.set_option("x2_R", 0)
