@@ -144,7 +144,7 @@ int launch_kernel(swb_ctx* ctx, const PassParams& Pin, long long items, int ctas
 }
 
 // packed 16x2 phase-1 kernel (swb_x2.cuh): R packed rows per lane, 64R rows per item
-constexpr int kX2R[] = {8, 12, 16};
+constexpr int kX2R[] = {8, 10, 12, 14, 16};
 
 template <int R>
 int dispatch_x2_R(swb_ctx* ctx, const PassParams* P, long long items, int ctas_per_sm,
@@ -158,7 +158,9 @@ int dispatch_x2(swb_ctx* ctx, int R, const PassParams* P, long long items, int c
                 int* occ_out) {
   switch (R) {
     case 8: return dispatch_x2_R<8>(ctx, P, items, ctas_per_sm, occ_out);
+    case 10: return dispatch_x2_R<10>(ctx, P, items, ctas_per_sm, occ_out);
     case 12: return dispatch_x2_R<12>(ctx, P, items, ctas_per_sm, occ_out);
+    case 14: return dispatch_x2_R<14>(ctx, P, items, ctas_per_sm, occ_out);
     case 16: return dispatch_x2_R<16>(ctx, P, items, ctas_per_sm, occ_out);
     default: break;
   }
@@ -243,8 +245,8 @@ Shape choose_shape(swb_ctx* ctx, const std::vector<PassReq*>& jobs, bool local, 
       strips += sj;
       chain = std::max(chain, (long long)r->n2 + (x2 ? 128LL : 64LL) * sj);
     }
-    // integer-ALU cycles per warp-step: 5.7 per row (x2: 2.7 per packed row pair)
-    const double alu = x2 ? 2.0 * (2.9 * R + 16.0) : 2.0 * (5.7 * R + 10.0);
+    // integer-ALU cycles per warp-step: 5.7 per row (x2: 5.5 per packed row pair)
+    const double alu = x2 ? 2.0 * (5.5 * R + 6.0) : 2.0 * (5.7 * R + 10.0);
     const double lat = 1.7 * alu;
     const long long w_need = (strips + smsp - 1) / smsp;
     const int w = (int)std::min<long long>(w_need, occ);
@@ -297,7 +299,7 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
                       r.n1, r.n2);
   }
   // packed 16x2 fast path eligibility (swb_x2.cuh header)
-  bool x2_scheme = sc.k <= 4 && ctx->x2_enabled;
+  bool x2_scheme = sc.k <= 4 && ctx->x2_enabled && 95 * std::max(sc.max_sub, 0) <= 1021;
   for (int b = 0; b < sc.k && x2_scheme; ++b)
     for (int a = 0; a < sc.k; ++a) {
       const int v = (int)(int8_t)((sc.tlo[b] >> (8 * a)) & 0xff);

@@ -3,10 +3,10 @@
 // One warp runs a 64-lane virtual pipeline: the low 16 bits of every register
 // hold strip A (rows [R0, R0 + 32R)), the high 16 bits strip B (the next 32R
 // rows).  Lane l processes column s - l of A and column s - l - 32 of B at step
-// s, so B's lane 0 consumes A's lane 31 output of the previous step (one extra
-// shuffle) and B's bottom row is the item's output to the next warp.  Every DP
-// instruction is a DPX S16x2 op or a carry-free 32-bit IMAD on two 16-bit
-// fields, i.e. two cells per instruction:
+// s, so B's lane 0 consumes A's lane 31 output of the previous step and B's
+// bottom row is the item's output to the next warp.  Every DP instruction is a
+// DPX S16x2 op or a carry-free 32-bit IMAD on two 16-bit fields, i.e. two
+// cells per instruction (5 ALU-pipe + 2 FMA-pipe instructions per cell pair):
 //
 //   s   = PRMT(T[colA], T[colB], sel_r)           two zero-extended bytes (sub + go + ge)
 //   ds  = IMAD(hm_diag, 1, s)                     packed add, no carry (fields in [0, 32767])
@@ -25,6 +25,23 @@
 // every value on an optimal path stays exact.  The base is
 // re-chosen every 32 steps from the warp maximum and the incoming top row.
 //
+// Endpoint tracking (reference TRACK_MIN: largest score, then smallest row,
+// then smallest column) uses packed 16-bit keys relative to a per-block
+// reference V_ref = max(V, M + 95 max_sub - 1022) of each lane half, V its
+// running best and M the warp maximum at the block start:
+//   key = 32 * max(hm - V_ref + 1, 0) + (31 - r).
+// No cell of the 95-column block exceeds M + 95 max_sub, so keys stay below
+// 32768 and are exact; cells below V_ref are below M, hence strictly below the
+// final best, and cannot be the endpoint.  Each step folds its keys into a
+// running maximum that is also stored to shared memory; at the block end a
+// half whose maximum beats its best's key (32 + rank, or 31 when V_ref > V)
+// binary-searches the stored maxima for the first step that reached it.
+// Requires 95 max_sub <= 1021.
+//
+// The producer's row enters through lane 0 as IMAD(shfl(x), 65536, top): the
+// shuffle from lane 31 moves A's bottom into B's half while the top value
+// fills A's half; the other lanes compute IMAD(shfl(x), 1, 0).
+//
 // Scope: local passes, TRACK_MIN, no band, no final rows, alphabets of <= 4
 // codes with 0 <= sub + go + ge <= 127.  Everything else uses run_strip.
 #pragma once
@@ -35,10 +52,13 @@ namespace swb {
 
 constexpr int kX2Off = 1024;     // rel value of the floor
 constexpr int kX2Span = 26000;   // max - base kept below this
+constexpr int kX2KeyRoom = 1022; // key t field stays <= 1023
 
 struct WarpSmemX2 {
-  int4 ring[128];  // per column c: (top hm abs, top F abs, profile word, -) at [c & 127]
-  int2 out[32];
+  uint32_t prof[96];  // profile word of column s0 - 64 + w (0 outside [0, n2))
+  int2 tz[64];        // [0, 32): rel (h, f) of the producer's row at column s0 + k; [32, 64): 0
+  uint2 out[32];      // raw packed (hm, F) of lane 31 at step k (B's bottom row)
+  uint32_t trk[32][32];  // [k][lane]: running packed key maximum after step k
 };
 
 __device__ __forceinline__ uint32_t vimax3_2(uint32_t a, uint32_t b, uint32_t c) {
@@ -46,6 +66,9 @@ __device__ __forceinline__ uint32_t vimax3_2(uint32_t a, uint32_t b, uint32_t c)
 }
 __device__ __forceinline__ uint32_t viaddmax_2(uint32_t a, uint32_t b, uint32_t c) {
   return (uint32_t)__viaddmax_s16x2((int)a, (int)b, (int)c);
+}
+__device__ __forceinline__ uint32_t viaddmax_relu_2(uint32_t a, uint32_t b, uint32_t c) {
+  return (uint32_t)__viaddmax_s16x2_relu((int)a, (int)b, (int)c);
 }
 __device__ __forceinline__ uint32_t pack2(int lo, int hi) {
   return ((uint32_t)lo & 0xffffu) | ((uint32_t)hi << 16);
@@ -56,9 +79,10 @@ __device__ __forceinline__ int clamp_rel(long long v) {
   return v < 0 ? 0 : (v > 32767 ? 32767 : (int)v);
 }
 
-template <int R, bool TRK_ANY>
+template <int R>
 __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& Jg, int s,
                                           WarpSmemX2* sm, const uint32_t* __restrict__ tw_s) {
+  static_assert(R <= 32, "rank field is 5 bits");
   const JobDev J = Jg;
   const int lane = threadIdx.x & 31;
   const int goe = P.goe, ge = P.ge;
@@ -81,12 +105,26 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     const uint32_t b = (ib < n1) ? 4u + (uint32_t)J.rows[(long long)ib * J.rstep] : 8u;
     sel[r] = a | ((a | 8u) << 4) | (b << 8) | ((b | 8u) << 12);
   }
+  // Every profile word an inactive half may read must be a valid one: a byte
+  // >= 128 would be sign-replicated by PRMT and its carry in the packed IMAD
+  // add would reach the other half.
+  for (int q = lane; q < 96; q += 32) sm->prof[q] = 0u;
+  sm->tz[32 + lane] = make_int2(0, 0);
+  __syncwarp();
 
   const uint32_t FLOOR2 = pack2(kX2Off, kX2Off);
   const uint32_t ZERO2 = 0u;
   const uint32_t NGE2 = pack2(-ge, -ge);
   const uint32_t NGOE2 = pack2(-goe, -goe);
   const int NGOE32 = -(goe * 65536 + goe);  // carry-free packed subtract of goe
+  const int k32 = P.key_mul;
+  const int up_mul = lane == 0 ? 65536 : 1;
+  const int src_lane = (lane + 31) & 31;
+  const int tz_off = lane == 0 ? 0 : 32;
+  uint32_t rk[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) rk[r] = (uint32_t)(31 - r) * 0x10001u;
+
   int base = 0;
   // local left border: H = 0 -> hm = -goe; E = max(NEG - ge, hm) = hm
   const uint32_t hm0 = pack2(kX2Off - goe, kX2Off - goe);
@@ -100,9 +138,24 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
   uint32_t diag = hm0;
   uint32_t out_hm = hm0, out_f = 0u;
 
-  int bkeyA = (-goe) * 32 + 31, bkeyB = (-goe) * 32 + 31;
+  // running best per half: hm value (absolute), rank 31 - r, column
+  int vA = -goe, vB = -goe, rkA = 31, rkB = 31;
   int bjA = -1, bjB = -1;
-  const int k32 = P.key_mul;
+  // per-block key frame: V_ref per half, 1 - V_ref(rel) and the best's key
+  long long vrA = 0, vrB = 0;
+  uint32_t nv2 = 0u, kb2 = 0u, bk2 = 0u;
+  auto set_frame = [&](long long mabs_w) {
+    const long long lowv = mabs_w + 95LL * P.max_sub - kX2KeyRoom;
+    vrA = vA > lowv ? vA : lowv;
+    vrB = vB > lowv ? vB : lowv;
+    long long ra = vrA - base + kX2Off, rb = vrB - base + kX2Off;
+    ra = ra < 0 ? 0 : (ra > 32767 ? 32767 : ra);
+    rb = rb < 0 ? 0 : (rb > 32767 ? 32767 : rb);
+    nv2 = pack2(1 - (int)ra, 1 - (int)rb);
+    kb2 = pack2(vrA == vA ? 32 + rkA : 31, vrB == vB ? 32 + rkB : 31);
+    bk2 = kb2;
+  };
+
   int known_prog = 0, prune_seen = 0;
   int code_next = (lane < n2) ? (int)J.cols[(long long)lane * J.cstep] : 0;
   long long pruned_blocks = 0, exec_blocks = 0, wait_cycles = 0;
@@ -110,42 +163,31 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
   unsigned long long g0, gw = 0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
   const int s_end = n2 + 63;
-  // Every ring slot an inactive half may read must hold a valid profile word:
-  // a stale byte >= 128 would be sign-replicated by PRMT and its carry in the
-  // packed IMAD add would corrupt the other (active) half.
-#pragma unroll
-  for (int q = lane; q < 128; q += 32) sm->ring[q] = make_int4(-goe, SWB_NEG32, 0, 0);
-  __syncwarp();
 
   auto step = [&](const int k, const int st, const bool guard, uint32_t (&Hin)[R],
                   uint32_t (&Hout)[R], auto trk_tag) {
-    constexpr bool TRK = decltype(trk_tag)::value && TRK_ANY;
+    constexpr bool TRK = decltype(trk_tag)::value;
     const int colA = st - lane, colB = colA - 32;
-    const int4 ra = sm->ring[colA & 127];
-    const int4 rb = sm->ring[colB & 127];
-    uint32_t up_h = __shfl_up_sync(0xffffffffu, out_hm, 1);
-    uint32_t up_f = __shfl_up_sync(0xffffffffu, out_f, 1);
-    const uint32_t x_h = __shfl_sync(0xffffffffu, out_hm, 31);
-    const uint32_t x_f = __shfl_sync(0xffffffffu, out_f, 31);
-    if (lane == 0) {
-      const long long off = (long long)kX2Off - base;
-      up_h = pack2(clamp_rel((long long)ra.x + off), lo16(x_h));
-      up_f = pack2(clamp_rel((long long)ra.y + off), lo16(x_f));
-    }
-    const bool actA = colA >= 0 && colA < n2;
-    const bool actB = colB >= 0 && colB < n2;
+    const int2 tp = sm->tz[tz_off + k];
+    const uint32_t tl = sm->prof[64 - lane + k], th = sm->prof[32 - lane + k];
+    const uint32_t up_h =
+        (uint32_t)imad((int)__shfl_sync(0xffffffffu, out_hm, src_lane), up_mul, tp.x);
+    const uint32_t up_f =
+        (uint32_t)imad((int)__shfl_sync(0xffffffffu, out_f, src_lane), up_mul, tp.y);
+    const bool actA = !guard || (colA >= 0 && colA < n2);
+    const bool actB = !guard || (colB >= 0 && colB < n2);
     if (guard && !actA && !actB) {
 #pragma unroll
       for (int r = 0; r < R; ++r) Hout[r] = Hin[r];
+      if (TRK) sm->trk[k][lane] = bk2;
       return;
     }
     const uint32_t keep = guard ? ((actA ? 0u : 0xffffu) | (actB ? 0u : 0xffff0000u)) : 0u;
-    const uint32_t tl = (uint32_t)ra.z, th = (uint32_t)rb.z;
     uint32_t d = diag;
     diag = guard ? ((up_h & ~keep) | (diag & keep)) : up_h;
     uint32_t fv = up_f;
     uint32_t hab = up_h;
-    int cmA = INT32_MIN, cmB = INT32_MIN, kpA = INT32_MIN, kpB = INT32_MIN;
+    uint32_t cm = guard ? 0u : bk2, kp = 0u;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const uint32_t sv = prmt(tl, th, sel[r]);
@@ -160,42 +202,28 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
       Hout[r] = guard ? ((hm & ~keep) | (Hin[r] & keep)) : hm;
       hab = h2m;
       if (TRK) {
-        const int ka = imad(lo16(hm), k32, 31 - r);
-        const int kb = imad(hi16(hm), k32, 31 - r);
-        if (r & 1) {
-          cmA = __vimax3_s32(cmA, kpA, ka);
-          cmB = __vimax3_s32(cmB, kpB, kb);
-        } else if (r == R - 1) {
-          cmA = cmA > ka ? cmA : ka;
-          cmB = cmB > kb ? cmB : kb;
-        }
-        kpA = ka;
-        kpB = kb;
+        const uint32_t t = viaddmax_relu_2(hm, nv2, NGE2);  // any c <= 0: max(hm + nv, 0)
+        const uint32_t key = (uint32_t)imad((int)t, k32, (int)rk[r]);
+        if (r & 1) cm = vimax3_2(cm, kp, key);
+        else if (r == R - 1) cm = vimax3_2(cm, key, key);
+        kp = key;
       }
     }
     out_hm = Hout[R - 1];
     out_f = fv;
     if (TRK) {
-      const int kb_off = (base - kX2Off) * 32;
-      if (actA && cmA + kb_off > bkeyA) {
-        bkeyA = cmA + kb_off;
-        bjA = colA;
-      }
-      if (actB && cmB + kb_off > bkeyB) {
-        bkeyB = cmB + kb_off;
-        bjB = colB;
-      }
+      bk2 = guard ? vimax3_2(bk2, cm & ~keep, 0u) : cm;
+      sm->trk[k][lane] = bk2;
     }
-    if (lane == 31 && actB) {
-      const int off = base - kX2Off;
-      sm->out[k] = make_int2(hi16(out_hm) + off, hi16(out_f) + off);
-    }
+    if (lane == 31 && actB) sm->out[k] = make_uint2(out_hm, out_f);
   };
 
   for (int s0 = 0; s0 < s_end; s0 += 32) {
-    // (1) stage the producer's bottom row and profile words for [s0, s0+32)
+    // (1) wait for and read the producer's bottom row for [s0, s0+32); shift
+    //     the profile window and stage the new columns' words
+    const int c = s0 + lane;
+    int top_h = -goe, top_f = SWB_NEG32;  // local top border: H = 0, F = -inf
     {
-      const int c = s0 + lane;
       const int code = code_next;
       const int pb_now = J.prune == 1 ? ld_relaxed(J.prune_best) : 0;
       {
@@ -217,22 +245,20 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
           known_prog = ld_acquire(up_progress);
         }
       }
-      if (c < n2) {
-        int th = -goe, tf = SWB_NEG32;  // local top border: H = 0, F = -inf
-        if (s > 0) {
-          const int2 v = __ldcg(inbuf + c);
-          th = v.x;
-          tf = v.y;
-        }
-        sm->ring[c & 127] = make_int4(th, tf, (int)tw_s[code], 0);
-      } else {
-        sm->ring[c & 127] = make_int4(-goe, SWB_NEG32, 0, 0);
+      if (s > 0 && c < n2) {
+        const int2 v = __ldcg(inbuf + c);
+        top_h = v.x;
+        top_f = v.y;
       }
-      prune_seen = pb_now;
+      const uint32_t p1 = sm->prof[32 + lane], p2 = sm->prof[64 + lane];
       __syncwarp();
+      sm->prof[lane] = p1;
+      sm->prof[32 + lane] = p2;
+      sm->prof[64 + lane] = c < n2 ? tw_s[code] : 0u;
+      prune_seen = pb_now;
     }
 
-    // (1b) re-base: warp maximum over the state and the staged top row
+    // (1b) re-base: warp maximum over the state and the incoming top row
     int mrel = 0;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -240,34 +266,17 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     }
     mrel = __vimax3_s32(mrel, lo16(out_hm), hi16(out_hm));
     long long mabs = (long long)mrel + base - kX2Off;  // hm (H - go - ge), absolute
-    {
-      const int c = s0 + lane;
-      if (c < n2) {
-        const int tv = sm->ring[c & 127].x;
-        if ((long long)tv > mabs) mabs = tv;
-      }
-    }
+    if (c < n2 && (long long)top_h > mabs) mabs = top_h;
     const int mabs_w = __reduce_max_sync(0xffffffffu, (int)(mabs > INT32_MAX ? INT32_MAX : mabs));
     {
       long long nb = (long long)mabs_w + goe - kX2Span;
       if (nb < 0) nb = 0;
       if (nb != base) {
-        const int delta = (int)(nb - base);
-        const int dd = delta > 32767 ? 32767 : (delta < -32767 ? -32767 : delta);
-        // shift by -delta per field, clamping at rel 0 (a lower bound, see header)
-        uint32_t sh = pack2(-dd, -dd);
-        int rem = delta - dd;
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          H[r] = viaddmax_2(H[r], sh, ZERO2);
-          E[r] = viaddmax_2(E[r], sh, ZERO2);
-        }
-        diag = viaddmax_2(diag, sh, ZERO2);
-        out_hm = viaddmax_2(out_hm, sh, ZERO2);
-        out_f = viaddmax_2(out_f, sh, ZERO2);
-        while (rem != 0) {  // very large jumps (after long pruned runs)
-          const int d2 = rem > 32767 ? 32767 : (rem < -32767 ? -32767 : rem);
-          sh = pack2(-d2, -d2);
+        // shift by -(nb - base) per field, clamping at rel 0 (a lower bound, see header)
+        long long rem = nb - base;
+        while (rem != 0) {
+          const int d2 = rem > 32767 ? 32767 : (rem < -32767 ? -32767 : (int)rem);
+          const uint32_t sh = pack2(-d2, -d2);
 #pragma unroll
           for (int r = 0; r < R; ++r) {
             H[r] = viaddmax_2(H[r], sh, ZERO2);
@@ -281,6 +290,10 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
         base = (int)nb;
       }
     }
+    // the producer's row in this block's frame (lane 0 injects it at step k)
+    sm->tz[lane] = make_int2(clamp_rel((long long)top_h - base + kX2Off),
+                             clamp_rel((long long)top_f - base + kX2Off));
+    __syncwarp();
     const bool steady = (s0 >= 63) && (s0 + 32 <= n2);
 
     // (2) pruning / tracking decision on the 95-column skewed block
@@ -307,16 +320,13 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
       }
       // lane 0's next diagonal is the real top input of the block's last column
       diag = fill;
-      if (lane == 0) {
-        const int t = sm->ring[(s0 + 31) & 127].x;
-        diag = pack2(clamp_rel((long long)t - base + kX2Off), hf);
-      }
+      if (lane == 0) diag = pack2(sm->tz[31].x, hf);
       out_hm = fill;
       out_f = 0u;
-      sm->out[lane] = make_int2(-goe, SWB_NEG32);
-      __syncwarp();
     } else {
       ++exec_blocks;
+      const bool trk_on = !steady || track_block;
+      if (trk_on) set_frame(mabs_w);
       using T1 = std::integral_constant<bool, true>;
       using T0 = std::integral_constant<bool, false>;
       if (steady && !track_block) {
@@ -339,12 +349,39 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
         }
       }
       __syncwarp();
+      if (trk_on && bk2 != kb2) {
+        // a strictly better cell in at least one half: first step reaching it
+        auto resolve = [&](bool hiHalf, int key, int colbase, int& v, int& rk_, int& bj,
+                           long long vref) {
+          int lo = 0;
+#pragma unroll
+          for (int stp = 16; stp > 0; stp >>= 1) {
+            const uint32_t w = sm->trk[lo + stp - 1][lane];
+            if ((hiHalf ? hi16(w) : lo16(w)) < key) lo += stp;
+          }
+          v = (int)(vref + (key >> 5) - 1);
+          rk_ = key & 31;
+          bj = colbase + lo;
+        };
+        const int ka = lo16(bk2), kbh = hi16(bk2);
+        if (ka > lo16(kb2)) resolve(false, ka, s0 - lane, vA, rkA, bjA, vrA);
+        if (kbh > hi16(kb2)) resolve(true, kbh, s0 - lane - 32, vB, rkB, bjB, vrB);
+      }
     }
+    __syncwarp();
 
     // (4) flush B's bottom row for columns [s0 - 63, s0 - 31) and publish
     {
-      const int c = s0 - 63 + lane;
-      if (c >= 0 && c < n2) __stcg(outbuf + c, sm->out[lane]);
+      const int cf = s0 - 63 + lane;
+      if (cf >= 0 && cf < n2) {
+        int2 o = make_int2(-goe, SWB_NEG32);  // pruned block: the fill values
+        if (!skip) {
+          const uint2 raw = sm->out[lane];
+          const int off = base - kX2Off;
+          o = make_int2(hi16(raw.x) + off, hi16(raw.y) + off);
+        }
+        __stcg(outbuf + cf, o);
+      }
       __syncwarp();
       if (lane == 0) {
         int pub = s0 - 31;
@@ -355,23 +392,22 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
 
     // (5) running best for pruning
     if (J.prune == 1) {
-      const int bm = __reduce_max_sync(0xffffffffu, (bkeyA > bkeyB ? bkeyA : bkeyB) >> 5);
+      const int bm = __reduce_max_sync(0xffffffffu, vA > vB ? vA : vB);
       if (lane == 0 && bm > -goe) atomicMax(J.prune_best, bm + goe);
     }
   }
   if (lane == 0) st_release(my_progress, n2);
 
   // item result: best of both halves, then warp reduction (smallest (i, j) on ties)
-  int b = bkeyA >> 5, ii = -1, jj = -1;
+  int b = vA, ii = -1, jj = -1;
   if (bjA >= 0) {
-    ii = rowA + (31 - (bkeyA & 31));
+    ii = rowA + (31 - rkA);
     jj = bjA;
   }
   if (bjB >= 0) {
-    const int bb = bkeyB >> 5;
-    const int ib = rowB + (31 - (bkeyB & 31));
-    if (ii < 0 || bb > b || (bb == b && (ib < ii || (ib == ii && bjB < jj)))) {
-      b = bb;
+    const int ib = rowB + (31 - rkB);
+    if (ii < 0 || vB > b || (vB == b && (ib < ii || (ib == ii && bjB < jj)))) {
+      b = vB;
       ii = ib;
       jj = bjB;
     }
@@ -427,7 +463,7 @@ __global__ void __launch_bounds__(256, 1) pass_kernel_x2(const PassParams P) {
       if (P.jobs[mid].item_base <= item) lo = mid;
       else hi = mid - 1;
     }
-    run_strip_x2<R, true>(P, P.jobs[lo], (int)(item - P.jobs[lo].item_base), sm, tw_s);
+    run_strip_x2<R>(P, P.jobs[lo], (int)(item - P.jobs[lo].item_base), sm, tw_s);
   };
   if (P.group > 0) {
     const int w = (int)(blockDim.x >> 7);
