@@ -10,9 +10,10 @@ score pass with endpoint (score_only).  A step is one full score pass.
   e2e       the same metric through the public API score_only(Sequence, ...)
             with host buffers: H2D of both sequences, device reverse copies,
             the pass and the D2H of the result inside the timed region.
-  roofline  integer/DPX issue roofline of the pass kernel: 6 integer-pipe ops
-            per executed cell against the chip DPX issue rate
-            measured live by swb_measure_int_peak.
+  roofline  integer/DPX issue roofline of the pass kernel: ALU-pipe instructions
+            per executed cell (packed 16x2 kernel: 5 per cell pair = 2.5; 32-bit
+            kernel: 6) against the chip DPX issue rate measured
+            live by swb_measure_int_peak.
   cpu_baseline  the CPU oracle port (oracle/, C + OpenMP block wavefront, a
             restatement of the reference engine) on a bounded window of the
             same pair, all host threads.
@@ -40,7 +41,11 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 N_DEFAULT = 1_000_000
-OPS_PER_CELL = 6  # PRMT + 4 VIADDMNMX + running max
+# ALU-pipe instructions per cell of the recurrence:
+#   lane32     PRMT + 4 VIADDMNMX + running max                       = 6
+#   packed16x2 PRMT + VIMNMX3 + 3 VIADDMNMX per two cells (S16x2)   = 2.5
+OPS_PER_CELL = {"lane32": 6.0, "packed16x2": 2.5}
+DTYPE = {"lane32": "int32", "packed16x2": "int16x2"}
 THROTTLE_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
                  0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
                  0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
@@ -247,12 +252,12 @@ def run_multi(args, rank, world, local, dist):
     value = cells * args.steps / (total_ms * 1e-3) / 1e9
     if rank == 0:
         exec_cells = sum(cells_all)
-        achieved = exec_cells * OPS_PER_CELL / (total_ms / args.steps * 1e-3) / 1e12
+        achieved = exec_cells * OPS_PER_CELL[res.kernel] / (total_ms / args.steps * 1e-3) / 1e12
         line = {
             "metric": "GCUPS (score pass, full-matrix cells / time)", "value": value,
             "unit": "GCUPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "vs_baseline": None, "dtype": DTYPE[res.kernel], "data": "synthetic",
             "config": {"workload": f"one alignment: {a.size} x {b.size} homologous pair "
                                    f"({args.n} x {args.n} cells per GPU), score + endpoint pass",
                        "n1": int(a.size), "n2": int(b.size), "prune": True,
@@ -376,13 +381,15 @@ def main():
 
     # -- roofline -------------------------------------------------------------------
     exec_cells = res.cells_executed
-    achieved = exec_cells * OPS_PER_CELL / (kernel_ms * 1e-3) / 1e12
+    opc = OPS_PER_CELL[res.kernel]
+    achieved = exec_cells * opc / (kernel_ms * 1e-3) / 1e12
     peak_t = peak["viaddmnmx"] / 1e12
     strips = (a.size + 1023) // 1024
     roofline = {"bound": "int", "achieved": achieved, "peak": peak_t, "unit": "Tops/s",
                 "frac": achieved / peak_t, "traffic": None,
                 "peak_source": "live swb_measure_int_peak (VIADDMNMX issue rate, all SMs)",
-                "ops_per_cell": OPS_PER_CELL, "cells_executed": exec_cells,
+                "ops_per_cell": opc, "kernel": res.kernel, "rows_per_lane": res.rows_per_lane,
+                "cells_executed": exec_cells,
                 "gcups_executed": exec_cells / (kernel_ms * 1e-3) / 1e9,
                 "kernel_ms": kernel_ms, "pruned_fraction": res.pruned_blocks / max(1, res.total_blocks)}
     prof = ROOT / "profiles" / "r01_traffic.json"
@@ -401,7 +408,7 @@ def main():
             "metric": "GCUPS (score pass, full-matrix cells / time)", "value": value,
             "unit": "GCUPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "vs_baseline": None, "dtype": DTYPE[res.kernel], "data": "synthetic",
             "config": {"workload": "C2: 1 Mbp x 1 Mbp homologous DNA pair (mutate 10%, seed 1002), "
                                    "score + endpoint forward pass" if args.n == N_DEFAULT and
                                    not args.unrelated else

@@ -46,7 +46,8 @@ class PassDesc(ctypes.Structure):
 class PassOut(ctypes.Structure):
     _fields_ = [("best_score", c_i64), ("best_i", c_i64), ("best_j", c_i64),
                 ("cells_executed", c_i64), ("tiles_total", c_i64), ("tiles_executed", c_i64),
-                ("tiles_pruned", c_i64), ("tiles_banded_out", c_i64), ("kernel_ms", ctypes.c_double)]
+                ("tiles_pruned", c_i64), ("tiles_banded_out", c_i64), ("kernel_ms", ctypes.c_double),
+                ("kernel", c_i32), ("rows_per_lane", c_i32)]
 
 
 class Subproblem(ctypes.Structure):

@@ -688,6 +688,8 @@ extern "C" int32_t swb_pass(swb_ctx* ctx, const swb_scheme* scheme, const swb_pa
     o.tiles_pruned = r.blocks_pruned;
     o.tiles_banded_out = std::max<long long>(0, r.blocks_total - r.blocks_exec - r.blocks_pruned);
     o.kernel_ms = r.kernel_ms;
+    o.kernel = r.x2 ? 1 : 0;
+    o.rows_per_lane = r.R;
     if (r.want_final) {
       std::vector<int32_t> th(r.n2), tf(r.n2);
       SWB_CUDA(cudaMemcpyAsync(th.data(), r.fin_h_dev, sizeof(int32_t) * r.n2,

@@ -193,6 +193,8 @@ class PassResult:
     banded_out_blocks: int
     cells_executed: int
     kernel_ms: float = 0.0
+    kernel: str = "lane32"     # "lane32" or "packed16x2" (which kernel carried the pass)
+    rows_per_lane: int = 0
 
 
 class Session:
@@ -278,7 +280,8 @@ class Session:
                 int(o.best_score), int(o.best_i), int(o.best_j),
                 fin[0] if fin else None, fin[1] if fin else None,
                 int(o.tiles_total), int(o.tiles_executed), int(o.tiles_pruned),
-                int(o.tiles_banded_out), int(o.cells_executed), float(o.kernel_ms)))
+                int(o.tiles_banded_out), int(o.cells_executed), float(o.kernel_ms),
+                "packed16x2" if o.kernel == 1 else "lane32", int(o.rows_per_lane)))
         # one launch carries all specs: count its time once
         if len(outs) > 1:
             self.kernel_ms -= sum(o.kernel_ms for o in outs[1:])

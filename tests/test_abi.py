@@ -32,7 +32,7 @@ def test_struct_layouts():
     assert ctypes.sizeof(_lib.Subproblem) == 48
     assert ctypes.sizeof(_lib.Crossing) == 40
     assert ctypes.sizeof(_lib.Scheme) == 4 * 68
-    assert ctypes.sizeof(_lib.PassOut) == 8 * 9
+    assert ctypes.sizeof(_lib.PassOut) == 8 * 9 + 4 * 2
 
 
 def test_version_without_device():
