@@ -46,6 +46,7 @@ struct swb_ctx {
   int claim_mode = 0;
   bool trace = false;
   int mm_prune = 1;
+  int job_major = 0;   // 1: claim strips job by job (no strip-major item map)
   int x2_enabled = 1;  // packed 16x2 kernel for eligible phase-1 passes
   int x2_R = 0;  // force the packed kernel's rows per lane (diagnostics)
   std::vector<unsigned long long> dbg_times;

@@ -87,7 +87,29 @@ struct PassParams {
   int32_t group;            // > 0: CTA-level claiming of `group` strips (see pass_kernel)
   int32_t mirror;           // CTA mode, single round, 2 warps/sub-partition: mirror pairs
   uint32_t tlo[8], thi[8];  // profile word per column code
+  const int2* item_map;     // claim order -> (job, strip); null: job-major by item_base
 };
+
+// Work item -> (job, strip).  Multi-job launches claim strips strip-major
+// across jobs (item_map) so that every pass of a level advances together and
+// a warp never holds a strip whose producer is far behind; a strip's producer
+// (strip s-1 of the same job) is always claimed earlier, so the persistent
+// launch stays deadlock-free.
+__device__ __forceinline__ int item_job(const PassParams& P, long long item, int* strip) {
+  if (P.item_map) {
+    const int2 m = P.item_map[item];
+    *strip = m.y;
+    return m.x;
+  }
+  int lo = 0, hi = P.njobs - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (P.jobs[mid].item_base <= item) lo = mid;
+    else hi = mid - 1;
+  }
+  *strip = (int)(item - P.jobs[lo].item_base);
+  return lo;
+}
 
 __device__ __forceinline__ int vmaxadd(int a, int b, int c) { return __viaddmax_s32(a, b, c); }
 
@@ -600,15 +622,8 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
 template <int R, bool LOCAL, int TRACK>
 __device__ __forceinline__ void run_item(const PassParams& P, long long item, WarpSmem* sm,
                                          const uint32_t* tlo_s, const uint32_t* thi_s) {
-  // locate the pass owning this item (jobs sorted by item_base)
-  int lo = 0, hi = P.njobs - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (P.jobs[mid].item_base <= item) lo = mid;
-    else hi = mid - 1;
-  }
-  const JobDev& J = P.jobs[lo];
-  const int s = (int)(item - J.item_base);
+  int s = 0;
+  const JobDev& J = P.jobs[item_job(P, item, &s)];
   if (J.want_final && s == J.nstrips - 1)
     run_strip<R, LOCAL, TRACK, true>(P, J, s, sm, tlo_s, thi_s);
   else

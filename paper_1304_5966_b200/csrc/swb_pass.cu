@@ -12,11 +12,17 @@
 
 using namespace swb;
 
-__global__ void fill2_kernel(int32_t* a, int32_t va, int32_t* b, int32_t vb, int64_t n) {
-  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
-       x += (int64_t)gridDim.x * blockDim.x) {
-    a[x] = va;
-    b[x] = vb;
+// Pre-fill the final rows of every job of one launch (cells the pass skips
+// keep the fill values): one launch for all jobs; blockIdx.x strides the
+// jobs, blockIdx.y splits long rows.
+__global__ void fill_finals_kernel(const swb::JobDev* __restrict__ jobs, int nj) {
+  for (int t = blockIdx.x; t < nj; t += gridDim.x) {
+    const swb::JobDev& J = jobs[t];
+    if (!J.want_final) continue;
+    for (int x = blockIdx.y * blockDim.x + threadIdx.x; x < J.n2; x += gridDim.y * blockDim.x) {
+      J.fin_h[x] = J.fill_h;
+      J.fin_f[x] = SWB_NEG32;
+    }
   }
 }
 
@@ -116,6 +122,8 @@ int launch_any(swb_ctx* ctx, K kern, const PassParams& Pin, long long items, int
     int fit = 0;
     SWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, kern, threads, 0));
     if (fit >= 1) {
+      // adjacent strips of one chain share a sub-partition: job-major order
+      P.item_map = nullptr;
       P.group = 4 * per_sm;
       P.mirror = (per_sm == 2 && items <= 8LL * ctx->sms && ctx->proto != 8) ? 1 : 0;
       // dynamic shared memory pins the layout to exactly one CTA per SM
@@ -299,7 +307,13 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
                       r.n1, r.n2);
   }
   // packed 16x2 fast path eligibility (swb_x2.cuh header)
-  bool x2_scheme = sc.k <= 4 && ctx->x2_enabled && 95 * std::max(sc.max_sub, 0) <= 1021;
+  // 95 max_sub <= 1021: 16-bit endpoint keys (swb_x2.cuh).  Window bound:
+  // neighbouring cells differ by at most go + ge + max_sub, so every value of a
+  // warp's window (<= 1024 rows + 96 columns, plus 32 columns of growth) lies
+  // within kX2Span of the window maximum and the relative frame never clamps one.
+  const long long ms = std::max(sc.max_sub, 0);
+  bool x2_scheme = sc.k <= 4 && ctx->x2_enabled && 95 * ms <= 1021 &&
+                   1120LL * (sc.goe + ms) + 32LL * ms + sc.goe <= 25000;
   for (int b = 0; b < sc.k && x2_scheme; ++b)
     for (int a = 0; a < sc.k; ++a) {
       const int v = (int)(int8_t)((sc.tlo[b] >> (8 * a)) & 0xff);
@@ -355,7 +369,8 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     size_t bytes = 256 * 8 + sizeof(JobDev) * nj + sizeof(int32_t) * total_strips +
                    sizeof(unsigned long long) * 5 * nj + sizeof(int32_t) * nj + 64 +
                    sizeof(int4) * total_strips + 24 * total_strips + sizeof(int2) * 2 * total_cols +
-                   sizeof(int32_t) * 2 * final_cols + 4096 + 256 * 8 * (size_t)nj;
+                   sizeof(int32_t) * 2 * final_cols + 4096 + 256 * 8 * (size_t)nj +
+                   sizeof(int2) * total_strips + 256;
     Arena A;
     A.base = (char*)swb_scratch(ctx->rowbuf, bytes);
     if (!A.base) return swb_fail(SWB_ECUDA, "out of device memory (%zu bytes of pass scratch)", bytes);
@@ -371,13 +386,14 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     unsigned long long* d_times = A.take<unsigned long long>(3 * total_strips);
     // host staging (pinned)
     size_t hbytes = sizeof(JobDev) * nj + sizeof(int4) * total_strips +
-                    sizeof(unsigned long long) * 5 * nj + 1024;
+                    sizeof(unsigned long long) * 5 * nj + sizeof(int2) * total_strips + 1024;
     char* hbase = (char*)swb_scratch_host(ctx->host_pinned, hbytes);
     if (!hbase) return swb_fail(SWB_ECUDA, "pinned host allocation failed");
     JobDev* h_jobs = reinterpret_cast<JobDev*>(hbase);
     int4* h_res = reinterpret_cast<int4*>(hbase + sizeof(JobDev) * nj);
     unsigned long long* h_cnt =
         reinterpret_cast<unsigned long long*>(hbase + sizeof(JobDev) * nj + sizeof(int4) * total_strips);
+    int2* h_map = reinterpret_cast<int2*>(h_cnt + 5 * nj);
 
     long long item = 0, strip_off = 0;
     for (int t = 0; t < nj; ++t) {
@@ -434,18 +450,31 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
       item += r.nstrips;
       strip_off += r.nstrips;
     }
+    // strip-major claim order across jobs (item_job in swb_kernels.cuh)
+    int2* d_map = nullptr;
+    if (nj > 1 && !ctx->job_major) {
+      d_map = A.take<int2>(total_strips);
+      long long q = 0;
+      int max_strips = 0;
+      for (int t = 0; t < nj; ++t) max_strips = std::max(max_strips, h_jobs[t].nstrips);
+      for (int st = 0; st < max_strips; ++st)
+        for (int t = 0; t < nj; ++t)
+          if (st < h_jobs[t].nstrips) h_map[q++] = make_int2(t, st);
+    }
     if (A.off > bytes) return swb_fail(SWB_ECUDA, "internal: pass arena overflow");
 
     SWB_CUDA(cudaMemcpyAsync(d_jobs, h_jobs, sizeof(JobDev) * nj, cudaMemcpyHostToDevice, ctx->stream));
+    if (d_map)
+      SWB_CUDA(cudaMemcpyAsync(d_map, h_map, sizeof(int2) * total_strips, cudaMemcpyHostToDevice,
+                               ctx->stream));
     SWB_CUDA(cudaMemsetAsync(A.base + zero_begin, 0, zero_end - zero_begin, ctx->stream));
-    for (int t = 0; t < nj; ++t) {
-      const PassReq& r = reqs[order[g0 + t]];
-      if (r.want_final) {
-        int blocks = (int)std::min<long long>((r.n2 + 255) / 256, 2048);
-        fill2_kernel<<<blocks, 256, 0, ctx->stream>>>(r.fin_h_dev, h_jobs[t].fill_h, r.fin_f_dev,
-                                                     SWB_NEG32, r.n2);
-        ctx->launches++;
-      }
+    bool any_final = false;
+    for (int t = 0; t < nj && !any_final; ++t) any_final = reqs[order[g0 + t]].want_final;
+    if (any_final) {
+      const int gx = std::min(nj, 8 * ctx->sms);
+      const int gy = std::max(1, std::min(64, 8 * ctx->sms / gx));
+      fill_finals_kernel<<<dim3(gx, gy), 256, 0, ctx->stream>>>(d_jobs, nj);
+      ctx->launches++;
     }
     SWB_CUDA(cudaGetLastError());
 
@@ -460,6 +489,7 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     P.max_sub = sc.max_sub;
     P.proto = ctx->proto;
     P.key_mul = 32;
+    P.item_map = d_map;
     memcpy(P.tlo, sc.tlo, sizeof(P.tlo));
     memcpy(P.thi, sc.thi, sizeof(P.thi));
 
@@ -574,6 +604,7 @@ extern "C" int64_t swb_get_option(swb_ctx* ctx, const char* name) {
   if (!strcmp(name, "max_ctas_per_sm")) return ctx->max_ctas_per_sm;
   if (!strcmp(name, "x2_R")) return ctx->x2_R;
   if (!strcmp(name, "x2")) return ctx->x2_enabled;
+  if (!strcmp(name, "job_major")) return ctx->job_major;
   if (!strcmp(name, "mm_prune")) return ctx->mm_prune;
   if (!strcmp(name, "claim_mode")) return ctx->claim_mode;
   if (!strcmp(name, "proto")) return ctx->proto;
@@ -593,6 +624,10 @@ extern "C" int32_t swb_set_option(swb_ctx* ctx, const char* name, int64_t value)
   }
   if (!strcmp(name, "x2")) {
     ctx->x2_enabled = (int)value;
+    return SWB_OK;
+  }
+  if (!strcmp(name, "job_major")) {
+    ctx->job_major = (int)value;
     return SWB_OK;
   }
   if (!strcmp(name, "mm_prune")) {

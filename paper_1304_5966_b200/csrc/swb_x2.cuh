@@ -19,10 +19,12 @@
 // Values are stored relative to a warp-wide base: rel = abs - base + 1024.
 // FLOOR (rel 1024) is abs max(0, base): with base = 0 it is the local-alignment
 // clamp at 0 exactly; with base > 0 it only raises values that lie more than
-// 26000 below the warp's maximum, which no true value in the warp's window can
-// (adjacent DP cells differ by at most max_sub + go + ge and the window is
-// 2048 rows x 95 columns), so every value stays a lower bound of the truth and
-// every value on an optimal path stays exact.  The base is
+// 26000 below the warp's maximum, which no true value in the warp's window can:
+// by induction over rows and columns, neighbouring cells of H (and E, F against
+// their H) differ by at most max_sub + go + ge, the window spans at most 1024
+// rows + 96 columns, and the host only selects this kernel when
+// 1120 (go + ge + max_sub) + 32 max_sub + go + ge <= 25000.  So no value is ever
+// clamped by the frame and every value is exact.  The base is
 // re-chosen every 32 steps from the warp maximum and the incoming top row.
 //
 // Endpoint tracking (reference TRACK_MIN: largest score, then smallest row,
@@ -457,13 +459,9 @@ __global__ void __launch_bounds__(256, 1) pass_kernel_x2(const PassParams P) {
   const int lane = threadIdx.x & 31;
   WarpSmemX2* sm = &wsm[warp];
   auto run = [&](long long item) {
-    int lo = 0, hi = P.njobs - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (P.jobs[mid].item_base <= item) lo = mid;
-      else hi = mid - 1;
-    }
-    run_strip_x2<R>(P, P.jobs[lo], (int)(item - P.jobs[lo].item_base), sm, tw_s);
+    int s = 0;
+    const int j = item_job(P, item, &s);
+    run_strip_x2<R>(P, P.jobs[j], s, sm, tw_s);
   };
   if (P.group > 0) {
     const int w = (int)(blockDim.x >> 7);

@@ -123,7 +123,17 @@ def collect_leaves(S: Session, root: np.ndarray, leaf_limit: int, band: bool,
                 stats["mm_leaves"] = stats.get("mm_leaves", 0) + int(frontier.shape[0])
             return frontier
         inner = np.flatnonzero(~leaf)
+        if stats is not None:
+            import time
+            t0, c0 = time.perf_counter(), S.cells
         kids = _split_level(S, frontier[inner], band)
+        if stats is not None:
+            sub = frontier[inner]
+            area = int(((sub["ei"] - sub["si"]) * (sub["ej"] - sub["sj"])).sum())
+            stats.setdefault("mm_level_stats", []).append(
+                {"subs": int(inner.size), "area": area, "cells": int(S.cells - c0),
+                 "wall_s": round(time.perf_counter() - t0, 4),
+                 "kernel_ms": round(float(getattr(S.ctx, "last_kernel_ms", 0.0)), 3)})
         # splice: every inner node becomes two consecutive entries
         width = np.where(leaf, 1, 2)
         pos = np.concatenate(([0], np.cumsum(width)[:-1]))

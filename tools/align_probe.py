@@ -29,7 +29,7 @@ for arg in [x for x in sys.argv[1:] if not x.startswith("--")]:
            "gcups_e2e": round(a.size * b.size / dt / 1e9, 1),
            **{k: (round(v, 3) if isinstance(v, float) else v) for k, v in rep.items()
               if k in ("phase_seconds", "mm_levels", "mm_leaves", "t_crossings", "t_leaves",
-                       "device_kernel_ms", "kernel_ms", "pruned_fraction")}}
+                       "device_kernel_ms", "kernel_ms", "pruned_fraction", "mm_level_stats")}}
     if "phase_seconds" in out:
         out["phase_seconds"] = [round(x, 3) for x in rep["phase_seconds"]]
     if check:
