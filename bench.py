@@ -217,7 +217,7 @@ def run_multi(args, rank, world, local, dist):
         torch.cuda.synchronize()
         dist.barrier()
         ctx.timer_start()
-        r = S.run([slab_spec(me, S.n2, ext_in, ext_out)])[0]
+        r = S.run([slab_spec(me, S.n1, S.n2, ext_in, ext_out)])[0]
         return r, ctx.timer_stop()
 
     with Session(ctx, a, b, scheme) as S:

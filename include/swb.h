@@ -122,6 +122,9 @@ typedef struct {
   uint64_t ext_in_progress;
   uint64_t ext_out_buf;
   uint64_t ext_out_progress;
+  /* rows of the whole pass below this slab (0 for a whole pass): the prune
+   * bounds count the rows a path can still take on the GPUs below. */
+  int64_t rows_after;
 } swb_pass_desc;
 
 /* PassResult (engine.py:120-131) minus the final rows (written in place). */

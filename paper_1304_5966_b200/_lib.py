@@ -40,7 +40,7 @@ class PassDesc(ctypes.Structure):
                 ("row_offset", c_i64), ("prune_target", c_i64), ("corner_i", c_i64),
                 ("corner_j", c_i64), ("ext_in_buf", ctypes.c_uint64),
                 ("ext_in_progress", ctypes.c_uint64), ("ext_out_buf", ctypes.c_uint64),
-                ("ext_out_progress", ctypes.c_uint64)]
+                ("ext_out_progress", ctypes.c_uint64), ("rows_after", c_i64)]
 
 
 class PassOut(ctypes.Structure):

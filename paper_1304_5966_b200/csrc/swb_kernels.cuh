@@ -68,7 +68,7 @@ struct JobDev {
                                  // [3] cycles spent waiting on the strip above, [4] strip cycles
   int32_t* prune_best;   // running best score (plain) for pruning
   int32_t row_offset;    // DP row of row 0 (row slab of a multi-GPU pass)
-  int32_t pad1;
+  int32_t rows_after;    // rows of the pass below this slab (prune bounds)
   int2* ext_in;          // strip 0 top input from the GPU above (null: top border)
   int32_t* ext_in_prog;
   int2* ext_out;         // last strip bottom row to the GPU below (null: local buffer)
@@ -471,7 +471,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       m = m > tv ? m : tv;
       m = __reduce_max_sync(0xffffffffu, m);
       const long long inm = (long long)m + goe;
-      const int rem_r = n1 - R0;
+      const int rem_r = n1 - R0 + J.rows_after;
       const int rem_c = n2 - (s0 - 31);
       const long long ms = P.max_sub;
       if (J.prune == 1) {

@@ -153,6 +153,7 @@ int launch_kernel(swb_ctx* ctx, const PassParams& Pin, long long items, int ctas
 
 // packed 16x2 phase-1 kernel (swb_x2.cuh): R packed rows per lane, 64R rows per item
 constexpr int kX2R[] = {8, 10, 12, 14, 16};
+constexpr int kX2SlabR = 16;  // multigpu.SLAB_ROWS_PER_LANE x 32 rows = 64 x 16
 
 template <int R>
 int dispatch_x2_R(swb_ctx* ctx, const PassParams* P, long long items, int ctas_per_sm,
@@ -321,7 +322,11 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     }
   for (PassReq& r : reqs)
     r.x2 = x2_scheme && r.local && r.track == kTrackMin && !r.has_band && !r.want_final &&
-           !r.ext_in && !r.ext_out && r.row_offset == 0 && r.prune <= 1 && r.force_R == 0;
+           r.prune <= 1 &&
+           // rows_per_lane forces the 32-bit kernel, except on row slabs where
+           // it only fixes the strip granularity (64 x kX2SlabR rows here)
+           (r.force_R == 0 || r.ext_in || r.ext_out) &&
+           (!r.ext_out || r.n1 % (64 * kX2SlabR) == 0);  // slab bottom row = item bottom row
   // one launch per (recurrence, tracking, kernel) class; rows-per-lane per class
   auto cls = [&](int q) {
     return (reqs[q].x2 ? 100 : 0) + (reqs[q].local ? 10 : 0) + reqs[q].track;
@@ -334,8 +339,11 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     while (b < order.size() && cls(order[b]) == cls(order[a])) js.push_back(&reqs[order[b++]]);
     Shape sh = choose_shape(ctx, js, js[0]->local, js[0]->track, js[0]->x2);
     if (js[0]->x2 && ctx->x2_R) sh.R = ctx->x2_R;
+    if (js[0]->x2)
+      for (PassReq* r : js)
+        if (r->ext_out) sh.R = kX2SlabR;  // slabs are cut in multiples of 64 x kX2SlabR rows
     for (PassReq* r : js) {
-      r->R = r->force_R ? r->force_R : sh.R;
+      r->R = (r->force_R && !r->x2) ? r->force_R : sh.R;
       cls_ctas[r - &reqs[0]] = sh.ctas_per_sm;
     }
     a = b;
@@ -425,6 +433,7 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
       J.ext_in_prog = r.ext_in_prog;
       J.ext_out = r.ext_out;
       J.ext_out_prog = r.ext_out_prog;
+      J.rows_after = (int32_t)r.rows_after;
       J.nstrips = r.nstrips;
       J.want_final = r.want_final ? 1 : 0;
       J.item_base = item;
@@ -699,6 +708,9 @@ extern "C" int32_t swb_pass(swb_ctx* ctx, const swb_scheme* scheme, const swb_pa
     r.ext_in_prog = reinterpret_cast<int32_t*>(d.ext_in_progress);
     r.ext_out = reinterpret_cast<int2*>(d.ext_out_buf);
     r.ext_out_prog = reinterpret_cast<int32_t*>(d.ext_out_progress);
+    if (d.rows_after < 0 || d.rows_after >= (1LL << 31))
+      return swb_fail(SWB_ERANGE, "rows_after out of range");
+    r.rows_after = d.rows_after;
     if ((r.ext_in || r.ext_out || r.row_offset) && r.has_band)
       return swb_fail(SWB_EUNSUPPORTED, "row slabs (multi-GPU) do not support a band");
     if ((r.ext_in == nullptr) != (r.ext_in_prog == nullptr) ||

@@ -32,6 +32,7 @@ struct PassReq {
   int32_t* ext_in_prog = nullptr;
   int2* ext_out = nullptr;
   int32_t* ext_out_prog = nullptr;
+  long long rows_after = 0;  // pass rows below this slab (prune bounds)
   // filled by swb_run_passes
   int R = 0;
   bool x2 = false;  // packed 16x2 phase-1 kernel

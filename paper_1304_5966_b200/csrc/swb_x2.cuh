@@ -45,7 +45,8 @@
 // fills A's half; the other lanes compute IMAD(shfl(x), 1, 0).
 //
 // Scope: local passes, TRACK_MIN, no band, no final rows, alphabets of <= 4
-// codes with 0 <= sub + go + ge <= 127.  Everything else uses run_strip.
+// codes with 0 <= sub + go + ge <= 127, whole passes or row slabs whose
+// rows are a multiple of 64R.  Everything else uses run_strip.
 #pragma once
 
 #include "swb_kernels.cuh"
@@ -96,6 +97,19 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
   int2* __restrict__ outbuf = J.buf[s & 1];
   int32_t* my_progress = J.progress + s;
   const int32_t* up_progress = s > 0 ? J.progress + (s - 1) : nullptr;
+  // multi-GPU row slab: item 0 consumes the slab above, the
+  // last item produces into the slab below through peer memory (sys scope)
+  const bool ext_in = (s == 0) && (J.ext_in != nullptr);
+  const bool ext_out = (s == J.nstrips - 1) && (J.ext_out != nullptr);
+  const bool has_top = s > 0 || ext_in;
+  if (ext_in) {
+    inbuf = J.ext_in;
+    up_progress = J.ext_in_prog;
+  }
+  if (ext_out) {
+    outbuf = J.ext_out;
+    my_progress = J.ext_out_prog;
+  }
 
   // selectors: byte0 <- T[colA] byte a, byte2 <- T[colB] byte b, bytes 1 and 3
   // replicate the (zero) sign of a profile byte; padding rows select zeros.
@@ -232,22 +246,22 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
         const int cn = c + 32;
         code_next = (cn < n2) ? (int)J.cols[(long long)cn * J.cstep] : 0;
       }
-      if (s > 0 && s0 < n2) {
+      if (has_top && s0 < n2) {
         const int need = (s0 + 32 < n2) ? s0 + 32 : n2;
         if (known_prog < need) {
-          if (ld_relaxed(up_progress) < need) {
+          if ((ext_in ? ld_relaxed_sys(up_progress) : ld_relaxed(up_progress)) < need) {
             const long long tw = clock64();
             unsigned long long a0, a1;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a0));
-            wait_progress(up_progress, need);
+            wait_progress(up_progress, need, ext_in);
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a1));
             gw += a1 - a0;
             wait_cycles += clock64() - tw;
           }
-          known_prog = ld_acquire(up_progress);
+          known_prog = ext_in ? ld_acquire_sys(up_progress) : ld_acquire(up_progress);
         }
       }
-      if (s > 0 && c < n2) {
+      if (has_top && c < n2) {
         const int2 v = __ldcg(inbuf + c);
         top_h = v.x;
         top_f = v.y;
@@ -303,7 +317,7 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     if (J.prune == 1 && steady) {
       const long long inm = (long long)mabs_w + goe;
       const long long ms = P.max_sub;
-      const int rem_r = n1 - R0;
+      const int rem_r = n1 - R0 + J.rows_after;
       const int rem_c = n2 - (s0 - 63);
       const long long bound = (inm > 0 ? inm : 0) + ms * (long long)(rem_r < rem_c ? rem_r : rem_c);
       skip = bound < (long long)prune_seen;
@@ -384,11 +398,15 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
         }
         __stcg(outbuf + cf, o);
       }
+      if (ext_out) __threadfence_system();
       __syncwarp();
       if (lane == 0) {
         int pub = s0 - 31;
         if (pub > n2) pub = n2;
-        if (pub > 0) st_release(my_progress, pub);
+        if (pub > 0) {
+          if (ext_out) st_release_sys(my_progress, pub);
+          else st_release(my_progress, pub);
+        }
       }
     }
 
@@ -398,7 +416,10 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
       if (lane == 0 && bm > -goe) atomicMax(J.prune_best, bm + goe);
     }
   }
-  if (lane == 0) st_release(my_progress, n2);
+  if (lane == 0) {
+    if (ext_out) st_release_sys(my_progress, n2);
+    else st_release(my_progress, n2);
+  }
 
   // item result: best of both halves, then warp reduction (smallest (i, j) on ties)
   int b = vA, ii = -1, jj = -1;

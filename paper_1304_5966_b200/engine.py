@@ -230,7 +230,7 @@ class Session:
 
     def desc(self, rows: tuple, cols: tuple, border: str, clamp: bool, track: int,
              band=None, prune=False, final=None, row_offset=0, ext_in=None,
-             ext_out=None, prune_target=0, corner=None) -> _lib.PassDesc:
+             ext_out=None, prune_target=0, corner=None, rows_after=0) -> _lib.PassDesc:
         """rows/cols = (offset, length, reversed) slices of seq1/seq2;
         row_offset/ext_in/ext_out describe a row slab of a multi-GPU pass
         (multigpu.py, include/swb.h)."""
@@ -252,6 +252,7 @@ class Session:
             d.final_row_h = final[0].ctypes.data
             d.final_row_f = final[1].ctypes.data
         d.row_offset = int(row_offset)
+        d.rows_after = int(rows_after)
         if ext_in is not None:
             d.ext_in_buf, d.ext_in_progress = int(ext_in[0]), int(ext_in[1])
         if ext_out is not None:

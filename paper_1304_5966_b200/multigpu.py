@@ -125,12 +125,14 @@ def ipc_import(ctx, handle: bytes) -> int:
     return int(p.value)
 
 
-def slab_spec(slab: Slab, n2: int, ext_in: tuple[int, int] | None,
+def slab_spec(slab: Slab, n1: int, n2: int, ext_in: tuple[int, int] | None,
               ext_out: tuple[int, int] | None, prune: bool = True) -> dict:
-    """Session.run() spec of one slab of a local score pass (phase1.py:44-85)."""
+    """Session.run() spec of one slab of a local score pass (phase1.py:44-85).
+    rows_after (the pass's rows below the slab) keeps the pruning bound of
+    phase1.py:55-59 sound for paths that continue on the GPUs below."""
     return dict(rows=(slab.row0, slab.rows, 0), cols=(0, n2, 0), border="local", clamp=True,
                 track=TRACK_MIN, prune=prune, row_offset=slab.row0,
-                ext_in=ext_in, ext_out=ext_out)
+                ext_in=ext_in, ext_out=ext_out, rows_after=n1 - slab.row1)
 
 
 def run_slabs_sequential(S, slabs: list[Slab], prune: bool = True):
@@ -145,7 +147,7 @@ def run_slabs_sequential(S, slabs: list[Slab], prune: bool = True):
         for g, slab in enumerate(slabs):
             ext_in = (bounds[g - 1].buf, bounds[g - 1].progress) if g > 0 else None
             ext_out = (bounds[g].buf, bounds[g].progress) if g + 1 < len(slabs) else None
-            r = S.run([slab_spec(slab, S.n2, ext_in, ext_out, prune)])[0]
+            r = S.run([slab_spec(slab, S.n1, S.n2, ext_in, ext_out, prune)])[0]
             results.append(r)
         merged = merge_best([(r.best_score, r.best_i, r.best_j) for r in results], TRACK_MIN)
         return merged, results

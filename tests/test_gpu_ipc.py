@@ -53,14 +53,14 @@ def _worker(rank, port, q):
         if rank == 0:
             hb, hp = handles[1]
             ext_out = (ipc_import(ctx, hb), ipc_import(ctx, hp))
-            r = S.run([slab_spec(slabs[0], S.n2, None, ext_out)])[0]
+            r = S.run([slab_spec(slabs[0], S.n1, S.n2, None, ext_out)])[0]
             dist.barrier()  # slab 0 complete before slab 1 starts
             ctx.set_option("rows_per_lane", 0)
             single = S.run([dict(rows=(0, S.n1, 0), cols=(0, S.n2, 0), border="local",
                                  clamp=True, track=1, prune=True)])[0]
         else:
             dist.barrier()
-            r = S.run([slab_spec(slabs[1], S.n2, (inbound.buf, inbound.progress), None)])[0]
+            r = S.run([slab_spec(slabs[1], S.n1, S.n2, (inbound.buf, inbound.progress), None)])[0]
             single = None
     got = [None, None]
     dist.all_gather_object(got, (r.best_score, r.best_i, r.best_j))
