@@ -125,6 +125,15 @@ typedef struct {
   /* rows of the whole pass below this slab (0 for a whole pass): the prune
    * bounds count the rows a path can still take on the GPUs below. */
   int64_t rows_after;
+  /* Tile bound maps of the (seq1, seq2) pair (swb_bounds_reset, DESIGN.md
+   * §3.6).  bound_write: 0 none, 1 record an upper bound of this pass's H per
+   * 1024 x 1024 forward tile into the forward map, 2 into the reverse map.
+   * bound_read: 0 none, 1 / 2 skip a block (prune kinds 2 and 3 only) when
+   * max(block inputs) + W max_sub + (map max over the block's tiles) +
+   * bound_offset < prune_target. */
+  int32_t bound_write;
+  int32_t bound_read;
+  int64_t bound_offset;
 } swb_pass_desc;
 
 /* PassResult (engine.py:120-131) minus the final rows (written in place). */
@@ -149,6 +158,13 @@ typedef struct {
   int64_t expected;
   int32_t start_vgap;
   int32_t end_vgap;
+  /* optional tile-bound pruning: when use_bounds != 0 and
+   * the pair's maps were filled by phases 1 and 2, prefix / suffix are the
+   * scores of the optimal path before (si, sj) and after (ei, ej). */
+  int32_t use_bounds;
+  int32_t pad;
+  int64_t prefix;
+  int64_t suffix;
 } swb_subproblem;
 
 /* find_crossing result (phase3.py:136-190). status 0 = ok, 1 = ScoreMismatch
@@ -183,6 +199,12 @@ int32_t swb_seq_release(swb_ctx* ctx, int32_t seq_id);
  * Run n independent passes in one persistent launch (run_wavefront x n). */
 int32_t swb_pass(swb_ctx* ctx, const swb_scheme* scheme, const swb_pass_desc* descs,
                  int32_t n, swb_pass_out* outs);
+
+/* --- tile bound maps ------------------------------------------------------------
+ * (Re)allocate and clear the forward and reverse tile maps of the pair
+ * (seq1, seq2): ceil(n1/1024) x ceil(n2/1024) int32 each.  One pair at a time
+ * per context; a later call for another pair replaces them. */
+int32_t swb_bounds_reset(swb_ctx* ctx, int32_t seq1, int32_t seq2);
 
 /* --- Myers-Miller level --------------------------------------------------------
  * For each subproblem (rows >= 2 required): run the upper forward and the

@@ -40,7 +40,8 @@ class PassDesc(ctypes.Structure):
                 ("row_offset", c_i64), ("prune_target", c_i64), ("corner_i", c_i64),
                 ("corner_j", c_i64), ("ext_in_buf", ctypes.c_uint64),
                 ("ext_in_progress", ctypes.c_uint64), ("ext_out_buf", ctypes.c_uint64),
-                ("ext_out_progress", ctypes.c_uint64), ("rows_after", c_i64)]
+                ("ext_out_progress", ctypes.c_uint64), ("rows_after", c_i64),
+                ("bound_write", c_i32), ("bound_read", c_i32), ("bound_offset", c_i64)]
 
 
 class PassOut(ctypes.Structure):
@@ -52,7 +53,8 @@ class PassOut(ctypes.Structure):
 
 class Subproblem(ctypes.Structure):
     _fields_ = [("si", c_i64), ("sj", c_i64), ("ei", c_i64), ("ej", c_i64), ("expected", c_i64),
-                ("start_vgap", c_i32), ("end_vgap", c_i32)]
+                ("start_vgap", c_i32), ("end_vgap", c_i32), ("use_bounds", c_i32), ("pad", c_i32),
+                ("prefix", c_i64), ("suffix", c_i64)]
 
 
 class Crossing(ctypes.Structure):
@@ -74,7 +76,7 @@ EXPORTS = (
     "swb_last_kernel_ms", "swb_launch_count", "swb_set_option", "swb_get_option", "swb_debug_stats",
     "swb_debug_times", "swb_timer_start", "swb_timer_stop", "swb_flush_l2",
     "swb_boundary_alloc", "swb_boundary_reset", "swb_boundary_free", "swb_ipc_export",
-    "swb_ipc_import", "swb_ipc_close",
+    "swb_ipc_import", "swb_ipc_close", "swb_bounds_reset",
 )
 
 _lib = None
@@ -108,6 +110,8 @@ def load() -> ctypes.CDLL:
         lib.swb_crossings.argtypes = [c_p, P(Scheme), c_i32, c_i32, P(Subproblem), c_i32, c_i32,
                                       P(Crossing), P(c_i64)]
         lib.swb_crossings.restype = c_i32
+        lib.swb_bounds_reset.argtypes = [c_p, c_i32, c_i32]
+        lib.swb_bounds_reset.restype = c_i32
         lib.swb_leaves.argtypes = [c_p, P(Scheme), c_i32, c_i32, P(Subproblem), c_i32, c_i32,
                                    c_p, c_p, c_p, c_p]
         lib.swb_leaves.restype = c_i32

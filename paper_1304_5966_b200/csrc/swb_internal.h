@@ -50,6 +50,11 @@ struct swb_ctx {
   int x2_enabled = 1;  // packed 16x2 kernel for eligible phase-1 passes
   int x2_R = 0;  // force the packed kernel's rows per lane (diagnostics)
   std::vector<unsigned long long> dbg_times;
+  // tile bound maps of one sequence pair
+  int bmap_seq1 = -1, bmap_seq2 = -1;
+  int bmap_nr = 0, bmap_nc = 0;
+  int bmaps_on = 1;             // option "bound_maps": 0 disables reads and writes
+  swb_buf bmap_fwd, bmap_rev;
   // scratch
   swb_buf jobs, rowbuf, progress, results, finals, misc, host_pinned, flush;
   cudaEvent_t tev0 = nullptr, tev1 = nullptr;

@@ -32,6 +32,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <climits>
 
 #include <type_traits>
 
@@ -73,6 +74,14 @@ struct JobDev {
   int32_t* ext_in_prog;
   int2* ext_out;         // last strip bottom row to the GPU below (null: local buffer)
   int32_t* ext_out_prog;
+  // tile bound maps: 1024 x 1024 tiles of the forward
+  // (seq1 x seq2) plane, int32 max(bound) + 2^30, -1 = never written (+inf)
+  int32_t* bmap_out;       // this pass writes an upper bound of its H per tile
+  const int32_t* bmap_in;  // this pass skips blocks the map proves useless
+  int32_t map_nr, map_nc;  // tiles
+  int32_t map_r0, map_rdir, map_c0, map_cdir;  // forward index of pass row/col 0, direction
+  int32_t bound_offset;    // skip iff in + W max_sub + map max + bound_offset < prune_target
+  int32_t pad2;
 };
 
 struct PassParams {
@@ -169,6 +178,106 @@ __device__ __forceinline__ void wait_progress(const int32_t* p, int need, bool s
     __nanosleep(ns);
     ns = ns < 4096 ? ns * 2 : 4096;
   }
+}
+
+// ---- Tile bound maps ------------------------------------
+// A pass may record, per 1024 x 1024 tile of the forward plane, an upper
+// bound of its H values (every block contributes max(inputs) + W max_sub, an
+// upper bound of every cell it covers), and a later pass may skip a block
+// when even the best continuation the map allows cannot reach its target.
+constexpr int kTileShift = 10;
+constexpr long long kBoundEnc = 1LL << 30;
+
+__device__ __forceinline__ int bound_enc(long long v) {
+  v += kBoundEnc;
+  return v < 0 ? 0 : (v > 0x7fffffffLL ? 0x7fffffff : (int)v);
+}
+
+// forward tile range [lo, hi] of pass rows (or columns) [a, b], a <= b
+__device__ __forceinline__ void tile_range(int base, int dir, int a, int b, int ntiles,
+                                           int& lo, int& hi) {
+  int fa = base + dir * a, fb = base + dir * b;
+  if (fa > fb) {
+    const int t = fa;
+    fa = fb;
+    fb = t;
+  }
+  lo = fa < 0 ? 0 : (fa >> kTileShift);
+  hi = fb < 0 ? 0 : (fb >> kTileShift);
+  if (lo > ntiles - 1) lo = ntiles - 1;
+  if (hi > ntiles - 1) hi = ntiles - 1;
+}
+
+// Per-warp writer: holds the (at most two) column tiles the current block
+// touches and flushes a tile with atomicMax once the blocks have moved past
+// it, so a strip issues ~2 atomics per 1024 columns.  State is warp-uniform.
+struct BoundWriter {
+  int t0 = -1, t1 = -1;
+  long long v0 = 0, v1 = 0;
+  int rt_lo = 0, rt_hi = -1;
+};
+
+__device__ __forceinline__ void bw_flush(const JobDev& J, const BoundWriter& w, int t,
+                                         long long v, int lane) {
+  if (t < 0) return;
+  const int rt = w.rt_lo + lane;
+  if (rt <= w.rt_hi) atomicMax(J.bmap_out + (long long)rt * J.map_nc + t, bound_enc(v));
+}
+
+__device__ __forceinline__ void bw_add(const JobDev& J, BoundWriter& w, int ta, int tb,
+                                       long long v, int lane) {
+  if (w.t0 >= 0 && w.t0 != ta && w.t0 != tb) {
+    bw_flush(J, w, w.t0, w.v0, lane);
+    w.t0 = -1;
+  }
+  if (w.t1 >= 0 && w.t1 != ta && w.t1 != tb) {
+    bw_flush(J, w, w.t1, w.v1, lane);
+    w.t1 = -1;
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int t = k ? tb : ta;
+    if (k && tb == ta) break;
+    if (t == w.t0) w.v0 = w.v0 > v ? w.v0 : v;
+    else if (t == w.t1) w.v1 = w.v1 > v ? w.v1 : v;
+    else if (w.t0 < 0) { w.t0 = t; w.v0 = v; }
+    else { w.t1 = t; w.v1 = v; }
+  }
+}
+
+__device__ __forceinline__ void bw_finish(const JobDev& J, BoundWriter& w, int lane) {
+  bw_flush(J, w, w.t0, w.v0, lane);
+  bw_flush(J, w, w.t1, w.v1, lane);
+  w.t0 = w.t1 = -1;
+}
+
+// Per-warp reader with a one-entry cache (the tile set changes every ~32 blocks).
+// Returns the decoded maximum over rows tiles [rt_lo, rt_hi] x columns tiles
+// [ta, tb], or LLONG_MAX when any of them was never written.
+struct BoundReader {
+  int ta = -2, tb = -2;
+  long long val = 0;
+  int rt_lo = 0, rt_hi = -1;
+};
+
+__device__ __forceinline__ long long br_get(const JobDev& J, BoundReader& r, int ta, int tb,
+                                            int lane) {
+  if (ta == r.ta && tb == r.tb) return r.val;
+  const int nct = tb - ta + 1;
+  const int n = (r.rt_hi - r.rt_lo + 1) * nct;
+  int m = -1;
+  bool unknown = false;
+  if (lane < n) {
+    const int rt = r.rt_lo + lane / nct, ct = ta + lane % nct;
+    m = __ldcg(J.bmap_in + (long long)rt * J.map_nc + ct);
+    unknown = m < 0;
+  }
+  unknown = __any_sync(0xffffffffu, unknown);
+  m = __reduce_max_sync(0xffffffffu, m);
+  r.ta = ta;
+  r.tb = tb;
+  r.val = unknown ? LLONG_MAX : (long long)m - kBoundEnc;
+  return r.val;
 }
 
 // Border values, engine.py:340-401.  I is a DP row, J a DP column.
@@ -273,6 +382,14 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     }
     return;
   }
+
+  BoundWriter bw;
+  BoundReader brd;
+  if (J.bmap_out) {
+    const int r_hi = (R0 + 32 * R < n1 ? R0 + 32 * R : n1) - 1;
+    tile_range(J.map_r0, J.map_rdir, R0, r_hi, J.map_nr, bw.rt_lo, bw.rt_hi);
+  }
+  if (J.bmap_in) tile_range(J.map_r0, J.map_rdir, R0 - 1, R0 + 32 * R, J.map_nr, brd.rt_lo, brd.rt_hi);
 
   // Row codes -> PRMT selectors (byte a, sign replicated into bytes 1..3).
   uint32_t sel[R];
@@ -463,14 +580,22 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     // (a cell below it can never be the final answer): most blocks of a
     // homologous pair run the untracked loop (no keys, no column max).
     bool track_block = true;
-    if (J.prune && steady) {
+    // input maximum of the block (state, values in flight, staged top row):
+    // with the band's and pruning's fills it bounds every cell of the block
+    // from above once max_sub per column is added
+    long long inm = 0;
+    if ((J.prune && steady) || J.bmap_out || (J.bmap_in && steady)) {
       int m = out_hm > diag ? out_hm : diag;
 #pragma unroll
       for (int r = 0; r < R; ++r) m = m > H[r] ? m : H[r];
-      const int tv = sm->ring[(s0 + lane) & 63].x;
-      m = m > tv ? m : tv;
+      if (s0 + lane < ce) {
+        const int tv = sm->ring[(s0 + lane) & 63].x;
+        m = m > tv ? m : tv;
+      }
       m = __reduce_max_sync(0xffffffffu, m);
-      const long long inm = (long long)m + goe;
+      inm = (long long)m + goe;
+    }
+    if (J.prune && steady) {
       const int rem_r = n1 - R0 + J.rows_after;
       const int rem_c = n2 - (s0 - 31);
       const long long ms = P.max_sub;
@@ -497,6 +622,25 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
         // + 2 go + ge: a completion may continue an open gap, and the two
         // halves of a gap join each charge one opening fee
         skip = inm + ub + 2LL * go + ge < (long long)J.prune_target;
+      }
+    }
+    // tile bound maps: skip when even the best continuation
+    // the map allows cannot reach the target; record this block's bound
+    if (J.bmap_in && steady && !skip) {
+      int ta, tb;
+      tile_range(J.map_c0, J.map_cdir, s0 - 32, s0 + 32, J.map_nc, ta, tb);
+      const long long mx = br_get(J, brd, ta, tb, lane);
+      if (mx != LLONG_MAX &&
+          inm + 63LL * P.max_sub + mx + J.bound_offset < (long long)J.prune_target)
+        skip = true;
+    }
+    if (J.bmap_out) {
+      const int lo = s0 - 31 > cb ? s0 - 31 : cb;
+      const int hi = s0 + 31 < ce - 1 ? s0 + 31 : ce - 1;
+      if (lo <= hi) {
+        int ta, tb;
+        tile_range(J.map_c0, J.map_cdir, lo, hi, J.map_nc, ta, tb);
+        bw_add(J, bw, ta, tb, (LOCAL && inm < 0 ? 0 : inm) + 63LL * P.max_sub, lane);
       }
     }
 
@@ -566,6 +710,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       if (lane == 0 && bm > -goe) atomicMax(J.prune_best, bm + goe);
     }
   }
+  if (J.bmap_out) bw_finish(J, bw, lane);
   if (lane == 0) {
     if (ext_out) st_release_sys(my_progress, ce);
     else st_release(my_progress, ce);

@@ -368,6 +368,13 @@ extern "C" int32_t swb_crossings(swb_ctx* ctx, const swb_scheme* scheme, int32_t
   std::vector<PassReq> reqs(2 * (size_t)n);
   std::vector<CombineDev> comb(n);
   long long off = 0;
+  // tile-bound pruning: slack for the junction gaps and the
+  // cell counted by both halves
+  const bool maps = ctx->bmaps_on && seq1 == ctx->bmap_seq1 && seq2 == ctx->bmap_seq2;
+  int min_sub = 0;
+  for (int a = 0; a < scheme->k; ++a)
+    for (int b = 0; b < scheme->k; ++b) min_sub = std::min(min_sub, scheme->sub[a * scheme->k + b]);
+  const long long slack = 4LL * sc.goe + 2LL * (std::max(sc.max_sub, 0) - min_sub);
   for (int t = 0; t < n; ++t) {
     const swb_subproblem& s = subs[t];
     const int rows = (int)(s.ei - s.si), cols = (int)(s.ej - s.sj);
@@ -412,6 +419,15 @@ extern "C" int32_t swb_crossings(swb_ctx* ctx, const swb_scheme* scheme, int32_t
       up.prune_target = dn.prune_target = s.expected;
       up.corner_i = dn.corner_i = rows;
       up.corner_j = dn.corner_j = cols;
+    }
+    up.prune_target = dn.prune_target = s.expected;
+    if (maps && s.use_bounds) {
+      // upper half: a cell c can be on an optimal S->T path only if
+      //   U(c) + R'(c) - suffix(T) + slack >= expected   (R' = phase-2 map)
+      swb_bind_maps(ctx, &up, s.si, midr, false, s.sj, cols, false, 0, 2, slack - s.suffix);
+      // lower half: L(c) + H_fwd(c) - prefix(S) + slack >= expected (phase-1 map)
+      swb_bind_maps(ctx, &dn, s.si + midr, rows - midr, true, s.sj, cols, true, 0, 1,
+                    slack - s.prefix);
     }
     CombineDev& c = comb[t];
     c.uh = up.fin_h_dev;

@@ -434,6 +434,16 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
       J.ext_out = r.ext_out;
       J.ext_out_prog = r.ext_out_prog;
       J.rows_after = (int32_t)r.rows_after;
+      J.bmap_out = r.bmap_out;
+      J.bmap_in = r.bmap_in;
+      J.map_nr = r.map_nr;
+      J.map_nc = r.map_nc;
+      J.map_r0 = r.map_r0;
+      J.map_rdir = r.map_rdir;
+      J.map_c0 = r.map_c0;
+      J.map_cdir = r.map_cdir;
+      J.bound_offset = (int32_t)std::max<long long>(std::min<long long>(r.bound_offset, 1LL << 29),
+                                                    -(1LL << 29));
       J.nstrips = r.nstrips;
       J.want_final = r.want_final ? 1 : 0;
       J.item_base = item;
@@ -608,12 +618,49 @@ static inline long long widen(int32_t v) {
   return v;
 }
 
+void swb_bind_maps(swb_ctx* ctx, PassReq* r, long long off1, long long len1, bool rev1,
+                   long long off2, long long len2, bool rev2, int write, int read,
+                   long long offset) {
+  int32_t* fwd = reinterpret_cast<int32_t*>(ctx->bmap_fwd.p);
+  int32_t* rev = reinterpret_cast<int32_t*>(ctx->bmap_rev.p);
+  r->map_nr = ctx->bmap_nr;
+  r->map_nc = ctx->bmap_nc;
+  r->map_r0 = (int)(rev1 ? off1 + len1 - 1 : off1);
+  r->map_rdir = rev1 ? -1 : 1;
+  r->map_c0 = (int)(rev2 ? off2 + len2 - 1 : off2);
+  r->map_cdir = rev2 ? -1 : 1;
+  r->bmap_out = write == 1 ? fwd : (write == 2 ? rev : nullptr);
+  r->bmap_in = read == 1 ? fwd : (read == 2 ? rev : nullptr);
+  r->bound_offset = offset;
+}
+
+extern "C" int32_t swb_bounds_reset(swb_ctx* ctx, int32_t seq1, int32_t seq2) {
+  SWB_API_BEGIN(ctx);
+  if (seq1 < 0 || seq1 >= (int)ctx->seqs.size() || !ctx->seqs[seq1].live || seq2 < 0 ||
+      seq2 >= (int)ctx->seqs.size() || !ctx->seqs[seq2].live)
+    return swb_fail(SWB_EINVAL, "bad sequence id");
+  const long long nr = std::max<long long>(1, (ctx->seqs[seq1].n + 1023) >> 10);
+  const long long nc = std::max<long long>(1, (ctx->seqs[seq2].n + 1023) >> 10);
+  const size_t bytes = sizeof(int32_t) * (size_t)nr * (size_t)nc;
+  void* f = swb_scratch(ctx->bmap_fwd, bytes);
+  void* r = f ? swb_scratch(ctx->bmap_rev, bytes) : nullptr;
+  if (!f || !r) return swb_fail(SWB_ECUDA, "out of device memory for bound maps (%zu bytes)", 2 * bytes);
+  SWB_CUDA(cudaMemsetAsync(f, 0xff, bytes, ctx->stream));  // -1: never written (+inf)
+  SWB_CUDA(cudaMemsetAsync(r, 0xff, bytes, ctx->stream));
+  ctx->bmap_seq1 = seq1;
+  ctx->bmap_seq2 = seq2;
+  ctx->bmap_nr = (int)nr;
+  ctx->bmap_nc = (int)nc;
+  SWB_API_END();
+}
+
 extern "C" int64_t swb_get_option(swb_ctx* ctx, const char* name) {
   if (!ctx || !name) return -1;
   if (!strcmp(name, "max_ctas_per_sm")) return ctx->max_ctas_per_sm;
   if (!strcmp(name, "x2_R")) return ctx->x2_R;
   if (!strcmp(name, "x2")) return ctx->x2_enabled;
   if (!strcmp(name, "job_major")) return ctx->job_major;
+  if (!strcmp(name, "bound_maps")) return ctx->bmaps_on;
   if (!strcmp(name, "mm_prune")) return ctx->mm_prune;
   if (!strcmp(name, "claim_mode")) return ctx->claim_mode;
   if (!strcmp(name, "proto")) return ctx->proto;
@@ -637,6 +684,10 @@ extern "C" int32_t swb_set_option(swb_ctx* ctx, const char* name, int64_t value)
   }
   if (!strcmp(name, "job_major")) {
     ctx->job_major = (int)value;
+    return SWB_OK;
+  }
+  if (!strcmp(name, "bound_maps")) {
+    ctx->bmaps_on = (int)value;
     return SWB_OK;
   }
   if (!strcmp(name, "mm_prune")) {
@@ -718,6 +769,17 @@ extern "C" int32_t swb_pass(swb_ctx* ctx, const swb_scheme* scheme, const swb_pa
       return swb_fail(SWB_EINVAL, "ext boundary needs both a buffer and a progress counter");
     if (r.row_offset < 0 || r.row_offset + r.n1 >= (1LL << 31))
       return swb_fail(SWB_ERANGE, "row_offset out of range");
+    if (d.bound_write < 0 || d.bound_write > 2 || d.bound_read < 0 || d.bound_read > 2)
+      return swb_fail(SWB_EINVAL, "bad bound map mode");
+    if ((d.bound_write || d.bound_read) && ctx->bmaps_on) {
+      if (d.seq1 != ctx->bmap_seq1 || d.seq2 != ctx->bmap_seq2)
+        return swb_fail(SWB_EINVAL, "bound maps were not reset for sequences (%d, %d)", d.seq1,
+                        d.seq2);
+      if (d.bound_read && d.prune != 2 && d.prune != 3)
+        return swb_fail(SWB_EINVAL, "bound_read needs a target (prune kind 2 or 3)");
+      swb_bind_maps(ctx, &r, d.off1, d.len1, d.rev1 != 0, d.off2, d.len2, d.rev2 != 0,
+                    d.bound_write, d.bound_read, d.bound_offset);
+    }
   }
   double ms = 0.0;
   rc = swb_run_passes(ctx, sc, reqs, &ms);

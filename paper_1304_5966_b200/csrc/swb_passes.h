@@ -33,6 +33,11 @@ struct PassReq {
   int2* ext_out = nullptr;
   int32_t* ext_out_prog = nullptr;
   long long rows_after = 0;  // pass rows below this slab (prune bounds)
+  // tile bound maps
+  int32_t* bmap_out = nullptr;
+  const int32_t* bmap_in = nullptr;
+  int map_nr = 0, map_nc = 0, map_r0 = 0, map_rdir = 1, map_c0 = 0, map_cdir = 1;
+  long long bound_offset = 0;
   // filled by swb_run_passes
   int R = 0;
   bool x2 = false;  // packed 16x2 phase-1 kernel
@@ -47,5 +52,8 @@ int swb_prepare_scheme(const swb_scheme* s, SchemeInt* out);
 int swb_check_range(const SchemeInt& sc, long long n1, long long n2);
 int swb_resolve_seq(swb_ctx* ctx, int32_t id, int64_t off, int64_t len, int32_t rev,
                     const uint8_t** base, int* step);
+void swb_bind_maps(swb_ctx* ctx, PassReq* r, long long off1, long long len1, bool rev1,
+                   long long off2, long long len2, bool rev2, int write, int read,
+                   long long offset);
 int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs,
                    double* kernel_ms_total);

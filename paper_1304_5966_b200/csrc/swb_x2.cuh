@@ -172,6 +172,12 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     bk2 = kb2;
   };
 
+  BoundWriter bw;  // tile bound map of this pass's H
+  if (J.bmap_out) {
+    const int r_hi = (R0 + 64 * R < n1 ? R0 + 64 * R : n1) - 1;
+    tile_range(J.map_r0, J.map_rdir, R0, r_hi, J.map_nr, bw.rt_lo, bw.rt_hi);
+  }
+
   int known_prog = 0, prune_seen = 0;
   int code_next = (lane < n2) ? (int)J.cols[(long long)lane * J.cstep] : 0;
   long long pruned_blocks = 0, exec_blocks = 0, wait_cycles = 0;
@@ -324,6 +330,17 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
       track_block = (inm > 0 ? inm : 0) + 95LL * ms >= (long long)prune_seen;
     }
 
+    if (J.bmap_out) {
+      const int lo = s0 - 63 > 0 ? s0 - 63 : 0;
+      const int hi = s0 + 31 < n2 - 1 ? s0 + 31 : n2 - 1;
+      if (lo <= hi) {
+        int ta, tb;
+        tile_range(J.map_c0, J.map_cdir, lo, hi, J.map_nc, ta, tb);
+        const long long inm = (long long)mabs_w + goe;
+        bw_add(J, bw, ta, tb, (inm > 0 ? inm : 0) + 95LL * P.max_sub, lane);
+      }
+    }
+
     if (skip) {
       ++pruned_blocks;
       // fill: H = 0 (hm = -goe), E/F = -inf (clamped at the floor)
@@ -416,6 +433,7 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
       if (lane == 0 && bm > -goe) atomicMax(J.prune_best, bm + goe);
     }
   }
+  if (J.bmap_out) bw_finish(J, bw, lane);
   if (lane == 0) {
     if (ext_out) st_release_sys(my_progress, n2);
     else st_release(my_progress, n2);

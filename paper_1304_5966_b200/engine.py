@@ -161,8 +161,18 @@ class DeviceContext:
         return float(self.lib.swb_last_kernel_ms(self.ptr))
 
 
+def bound_slack(scheme: ScoringScheme) -> int:
+    """Slack of the tile-bound tests (same formula as swb_crossings): junction
+    gaps and the cell counted by both halves of a split path."""
+    min_sub = min(0, int(np.asarray(scheme.matrix).min()))
+    return 4 * (scheme.gap_open + scheme.gap_extend) + 2 * (max(scheme.max_substitution_score, 0)
+                                                           - min_sub)
+
+
 SUBPROBLEM_DTYPE = np.dtype([("si", "<i8"), ("sj", "<i8"), ("ei", "<i8"), ("ej", "<i8"),
-                             ("expected", "<i8"), ("start_vgap", "<i4"), ("end_vgap", "<i4")])
+                             ("expected", "<i8"), ("start_vgap", "<i4"), ("end_vgap", "<i4"),
+                             ("use_bounds", "<i4"), ("pad", "<i4"), ("prefix", "<i8"),
+                             ("suffix", "<i8")])
 CROSSING_DTYPE = np.dtype([("mid_i", "<i8"), ("mid_j", "<i8"), ("upper", "<i8"),
                            ("lower", "<i8"), ("gap_join", "<i4"), ("status", "<i4")])
 assert SUBPROBLEM_DTYPE.itemsize == ctypes.sizeof(_lib.Subproblem)
@@ -214,6 +224,14 @@ class Session:
         self.kernel_ms = 0.0
         self.cells = 0
         self.target_prune = True  # phase-2 restricted searches skip hopeless blocks
+        self.bounds = False       # tile bound maps filled for this pair (reset_bounds)
+
+    def reset_bounds(self) -> None:
+        """Clear the pair's tile bound maps; phases 1 and 2 of
+        an align() fill them, phases 2 and 3 prune with them."""
+        _lib.check(self.ctx.lib.swb_bounds_reset(self.ctx.ptr, self.s1, self.s2),
+                   "swb_bounds_reset")
+        self.bounds = True
 
     def close(self):
         if self.s1 is not None:
@@ -230,7 +248,8 @@ class Session:
 
     def desc(self, rows: tuple, cols: tuple, border: str, clamp: bool, track: int,
              band=None, prune=False, final=None, row_offset=0, ext_in=None,
-             ext_out=None, prune_target=0, corner=None, rows_after=0) -> _lib.PassDesc:
+             ext_out=None, prune_target=0, corner=None, rows_after=0, bound_write=0,
+             bound_read=0, bound_offset=0) -> _lib.PassDesc:
         """rows/cols = (offset, length, reversed) slices of seq1/seq2;
         row_offset/ext_in/ext_out describe a row slab of a multi-GPU pass
         (multigpu.py, include/swb.h)."""
@@ -253,6 +272,8 @@ class Session:
             d.final_row_f = final[1].ctypes.data
         d.row_offset = int(row_offset)
         d.rows_after = int(rows_after)
+        d.bound_write, d.bound_read = int(bound_write), int(bound_read)
+        d.bound_offset = int(bound_offset)
         if ext_in is not None:
             d.ext_in_buf, d.ext_in_progress = int(ext_in[0]), int(ext_in[1])
         if ext_out is not None:

@@ -29,9 +29,11 @@ def prune_verdict(best_so_far: int, max_substitution_score: int, len1: int, len2
 
 
 def best_local(S: Session, prune: bool = True) -> tuple[ScoredEndpoint, PassResult]:
-    """Optimal local score and endpoint over the full matrix (phase1.py:44-85)."""
+    """Optimal local score and endpoint over the full matrix (phase1.py:44-85).
+    When the session's tile bound maps are on, the pass also records an upper
+    bound of H per tile for phases 2 and 3."""
     res = S.run([dict(rows=(0, S.n1, 0), cols=(0, S.n2, 0), border="local", clamp=True,
-                      track=TRACK_MIN, prune=prune)])[0]
+                      track=TRACK_MIN, prune=prune, bound_write=1 if S.bounds else 0)])[0]
     if res.best_score <= 0:
         return ScoredEndpoint(0, Coord(0, 0)), res
     return ScoredEndpoint(res.best_score, Coord(res.best_i + 1, res.best_j + 1)), res

@@ -11,7 +11,7 @@ import logging
 import math
 from dataclasses import dataclass
 
-from .engine import TRACK_MAX, Session
+from .engine import TRACK_MAX, Session, bound_slack
 from .errors import StartNotFound
 from .model import Coord, ScoringScheme
 
@@ -65,7 +65,7 @@ def oriented_interval(band: BandSpec, score: int, rows: int, cols: int,
 
 def restricted_search(S: Session, rows: tuple, cols: tuple, target: int, interval,
                       preopen_vgap: bool = False, track: int = TRACK_MAX,
-                      gap_tolerant: bool = False) -> tuple[int, int]:
+                      gap_tolerant: bool = False, bounds: bool = False) -> tuple[int, int]:
     """Origin-anchored pass returning the cell that attains `target`
     (phase2.py:82-138).  rows/cols are (offset, length, reversed) slices."""
     if gap_tolerant or preopen_vgap:
@@ -73,10 +73,15 @@ def restricted_search(S: Session, rows: tuple, cols: tuple, target: int, interva
     else:
         border = "restricted"
     # prune kind 2: blocks from which no path can reach `target` are skipped
-    # (sound: every cell attaining target keeps its exact value)
+    # (sound: every cell attaining target keeps its exact value).
+    # bounds: the phase-1 tile map bounds what the rest of the path (up to the
+    # start) can add, and this pass records its own tile map for phase 3 (§3.6).
+    extra = {}
+    if bounds and S.bounds and S.target_prune:
+        extra = dict(bound_read=1, bound_write=2, bound_offset=bound_slack(S.scheme))
     res = S.run([dict(rows=rows, cols=cols, border=border, clamp=False, track=track,
                       band=interval, prune=2 if S.target_prune else 0,
-                      prune_target=target)])[0]
+                      prune_target=target, **extra)])[0]
     if res.best_i < 0 or res.best_score != target:
         found = res.best_score if res.best_i >= 0 else "none"
         raise StartNotFound(f"no cell attains the known score {target} (best found: {found}); "
@@ -92,5 +97,5 @@ def locate_start(S: Session, end: Coord, score: int, band: BandSpec | None) -> C
     interval = None
     if band is not None:
         interval = oriented_interval(band, score, end.i, end.j, S.scheme)
-    ri, rj = restricted_search(S, (0, end.i, 1), (0, end.j, 1), score, interval)
+    ri, rj = restricted_search(S, (0, end.i, 1), (0, end.j, 1), score, interval, bounds=True)
     return Coord(end.i - ri - 1, end.j - rj - 1)

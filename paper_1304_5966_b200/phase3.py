@@ -55,11 +55,13 @@ def band_interval(rows: int, cols: int, score: int, scheme: ScoringScheme) -> tu
     return min(0, d) - pad, max(0, d) + pad
 
 
-def _as_array(subs: list[Subproblem]) -> np.ndarray:
+def _as_array(subs: list[Subproblem], use_bounds: bool = False) -> np.ndarray:
+    """Device form; prefix/suffix (scores before start and after end) start at
+    0 for the root, which is the whole alignment."""
     a = np.zeros(len(subs), dtype=SUBPROBLEM_DTYPE)
     for t, s in enumerate(subs):
         a[t] = (s.start.i, s.start.j, s.end.i, s.end.j, s.expected, int(s.start_vgap),
-                int(s.end_vgap))
+                int(s.end_vgap), int(use_bounds), 0, 0, 0)
     return a
 
 
@@ -106,6 +108,13 @@ def _split_level(S: Session, level: np.ndarray, band: bool) -> np.ndarray:
     dn["expected"] = res["lower"] + go * res["gap_join"].astype(np.int64)
     dn["start_vgap"] = res["gap_join"]
     dn["end_vgap"] = level["end_vgap"]
+    # optimal-path scores before / after each child (the children's expected
+    # scores partition the parent's), for tile-bound pruning
+    up["use_bounds"] = dn["use_bounds"] = level["use_bounds"]
+    up["prefix"] = level["prefix"]
+    up["suffix"] = level["suffix"] + dn["expected"]
+    dn["prefix"] = level["prefix"] + up["expected"]
+    dn["suffix"] = level["suffix"]
     return kids
 
 
@@ -198,7 +207,8 @@ def solve_rect(S: Session, sub: Subproblem, leaf_limit: int = DEFAULT_LEAF_LIMIT
     """Full op sequence of one known-score rectangle (phase3.py:250-286)."""
     import time
     t0 = time.perf_counter()
-    leaves = collect_leaves(S, _as_array([sub]), leaf_limit, band, stats)
+    leaves = collect_leaves(S, _as_array([sub], getattr(S, "bounds", False)), leaf_limit, band,
+                            stats)
     t1 = time.perf_counter()
     ops = solve_leaves(S, leaves, band)
     if stats is not None:

@@ -67,6 +67,7 @@ def align(seq1: Sequence, seq2: Sequence, scheme: ScoringScheme,
                 report.update(device_kernel_ms=S.kernel_ms, device_cells=S.cells)
             return out
         t0 = time.perf_counter()
+        S.reset_bounds()  # tile bound maps for phases 2 and 3
         scored, p1 = phase1.best_local(S, cfg.prune)
         t1 = time.perf_counter()
         _report_phase1(report, scored, p1, S)

@@ -6,7 +6,8 @@ from pathlib import Path
 
 from paper_1304_5966_b200 import _lib
 
-HEADER = Path(__file__).resolve().parents[1] / "include" / "swb.h"
+ROOT = Path(__file__).resolve().parents[1]
+HEADER = ROOT / "include" / "swb.h"
 
 
 def declared_functions():
@@ -27,12 +28,34 @@ def test_library_exports_all_header_symbols():
     assert set(_lib.EXPORTS) == set(declared_functions())
 
 
-def test_struct_layouts():
-    # field sizes mirror the C structs (x86-64 SysV)
-    assert ctypes.sizeof(_lib.Subproblem) == 48
-    assert ctypes.sizeof(_lib.Crossing) == 40
-    assert ctypes.sizeof(_lib.Scheme) == 4 * 68
-    assert ctypes.sizeof(_lib.PassOut) == 8 * 9 + 4 * 2
+STRUCTS = {"Subproblem": "swb_subproblem", "Crossing": "swb_crossing", "Scheme": "swb_scheme",
+           "PassOut": "swb_pass_out", "PassDesc": "swb_pass_desc", "IntPeak": "swb_int_peak"}
+
+
+def test_struct_layouts(tmp_path):
+    """ctypes mirrors of include/swb.h: size and every field offset equal what
+    the C compiler lays out (compiled here with gcc against the header)."""
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc") or "/usr/bin/gcc"
+    lines = ["#include <stddef.h>", "#include <stdio.h>", '#include "swb.h"', "int main(void) {"]
+    for py, c in STRUCTS.items():
+        st = getattr(_lib, py)
+        lines.append(f'printf("{py} %zu\\n", sizeof({c}));')
+        for name, _ in st._fields_:
+            lines.append(f'printf("{py}.{name} %zu\\n", offsetof({c}, {name}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run([gcc, "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
+    got = dict(l.split() for l in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                 check=True).stdout.splitlines())
+    for py in STRUCTS:
+        st = getattr(_lib, py)
+        assert int(got[py]) == ctypes.sizeof(st), py
+        for name, _ in st._fields_:
+            assert int(got[f"{py}.{name}"]) == getattr(st, name).offset, (py, name)
 
 
 def test_version_without_device():
