@@ -54,6 +54,7 @@ struct swb_ctx {
   int bmap_seq1 = -1, bmap_seq2 = -1;
   int bmap_nr = 0, bmap_nc = 0;
   int bmaps_on = 1;             // option "bound_maps": 0 disables reads and writes
+  int mm_R = 8;                 // rows per lane of range-limited Myers-Miller passes
   swb_buf bmap_fwd, bmap_rev;
   // scratch
   swb_buf jobs, rowbuf, progress, results, finals, misc, host_pinned, flush;

@@ -81,7 +81,9 @@ struct JobDev {
   int32_t map_nr, map_nc;  // tiles
   int32_t map_r0, map_rdir, map_c0, map_cdir;  // forward index of pass row/col 0, direction
   int32_t bound_offset;    // skip iff in + W max_sub + map max + bound_offset < prune_target
-  int32_t pad2;
+  int32_t range_offset;    // static ranges: tile useful iff fwd + rev + range_offset >= target
+  const int32_t* rmap_fwd; // static strip ranges from both maps (null: band only)
+  const int32_t* rmap_rev;
 };
 
 struct PassParams {
@@ -97,6 +99,8 @@ struct PassParams {
   int32_t mirror;           // CTA mode, single round, 2 warps/sub-partition: mirror pairs
   uint32_t tlo[8], thi[8];  // profile word per column code
   const int2* item_map;     // claim order -> (job, strip); null: job-major by item_base
+  int32_t warp_claim;       // 1: per-warp claiming even for few jobs (range-limited passes)
+  int32_t pad3;
 };
 
 // Work item -> (job, strip).  Multi-job launches claim strips strip-major
@@ -322,6 +326,56 @@ __device__ __forceinline__ void strip_range(const JobDev& J, int s, int& cb, int
   ce = (int)hi;
 }
 
+// Static strip range from the tile maps (Myers-Miller halves):
+// a cell can be on an optimal path of the subproblem only if its tile passes
+// fwd + rev + range_offset >= target (phase-1 H bound + phase-2 reverse bound);
+// the strip sweeps the hull of its useful tiles, everything else is fill.
+// Deterministic in the maps, so producer and consumer agree on each range.
+template <int R>
+__device__ __forceinline__ void static_range(const JobDev& J, int s, int& cb, int& ce) {
+  if (cb >= ce) return;
+  const int lane = threadIdx.x & 31;
+  const int r0 = s * 32 * R;
+  const int r1 = (r0 + 32 * R < J.n1 ? r0 + 32 * R : J.n1) - 1;
+  int rt_lo, rt_hi, ct_lo, ct_hi;
+  tile_range(J.map_r0, J.map_rdir, r0, r1, J.map_nr, rt_lo, rt_hi);
+  tile_range(J.map_c0, J.map_cdir, cb, ce - 1, J.map_nc, ct_lo, ct_hi);
+  int fmin = 0x7fffffff, fmax = -1;
+  for (int base = ct_lo; base <= ct_hi; base += 32) {
+    const int ct = base + lane;
+    bool useful = false;
+    if (ct <= ct_hi) {
+      for (int rt = rt_lo; rt <= rt_hi; ++rt) {
+        const long long k = (long long)rt * J.map_nc + ct;
+        const int a = __ldcg(J.rmap_fwd + k), b = __ldcg(J.rmap_rev + k);
+        if (a < 0 || b < 0 ||
+            (long long)a + b - 2 * kBoundEnc + J.range_offset >= (long long)J.prune_target)
+          useful = true;
+      }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, useful);
+    if (m) {
+      if (fmin == 0x7fffffff) fmin = base + __ffs(m) - 1;
+      fmax = base + 31 - __clz(m);
+    }
+  }
+  if (fmax < 0) {
+    ce = cb;
+    return;
+  }
+  const long long flo = (long long)fmin << kTileShift, fhi = (((long long)fmax + 1) << kTileShift) - 1;
+  long long lo, hi;  // pass columns
+  if (J.map_cdir > 0) {
+    lo = flo - J.map_c0;
+    hi = fhi - J.map_c0;
+  } else {
+    lo = J.map_c0 - fhi;
+    hi = J.map_c0 - flo;
+  }
+  if (lo > cb) cb = (int)(lo < ce ? lo : ce);
+  if (hi + 1 < ce) ce = (int)(hi + 1 > cb ? hi + 1 : cb);
+}
+
 struct WarpSmem {
   int4 ring[64];  // per column c: (top hm, top F, profile lo, profile hi) at [c & 63]
   int2 out[32];   // lane-31 outputs of the current 32-step block
@@ -354,6 +408,10 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
   strip_range<R>(J, s, cb, ce);
   int cbp = 0, cep = 0;
   if (s > 0) strip_range<R>(J, s - 1, cbp, cep);
+  if (J.rmap_fwd) {
+    static_range<R>(J, s, cb, ce);
+    if (s > 0) static_range<R>(J, s - 1, cbp, cep);
+  }
   const int2* __restrict__ inbuf = J.buf[(s + 1) & 1];  // written by strip s-1
   int2* __restrict__ outbuf = J.buf[s & 1];
   int32_t* my_progress = J.progress + s;

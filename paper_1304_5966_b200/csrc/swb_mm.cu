@@ -428,6 +428,16 @@ extern "C" int32_t swb_crossings(swb_ctx* ctx, const swb_scheme* scheme, int32_t
       // lower half: L(c) + H_fwd(c) - prefix(S) + slack >= expected (phase-1 map)
       swb_bind_maps(ctx, &dn, s.si + midr, rows - midr, true, s.sj, cols, true, 0, 1,
                     slack - s.prefix);
+      // static strip ranges: a tile can hold an optimal S->T cell only if
+      //   Hf(tile) + R'(tile) + slack - prefix(S) - suffix(T) >= expected
+      for (PassReq* q : {&up, &dn}) {
+        q->rmap_fwd = reinterpret_cast<const int32_t*>(ctx->bmap_fwd.p);
+        q->rmap_rev = reinterpret_cast<const int32_t*>(ctx->bmap_rev.p);
+        q->range_offset = slack - s.prefix - s.suffix;
+        // the pass is a chain along the path: its length grows with strip
+        // height (rows + lag per strip at R-row step cost), so short strips
+        if (!ctx->force_R && ctx->mm_R) q->force_R = ctx->mm_R;
+      }
     }
     CombineDev& c = comb[t];
     c.uh = up.fin_h_dev;

@@ -115,8 +115,8 @@ int launch_any(swb_ctx* ctx, K kern, const PassParams& Pin, long long items, int
   SWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, 0));
   if (per_sm < 1) return swb_fail(SWB_ECUDA, "pass kernel does not fit on an SM");
   if (ctas_per_sm > 0 && per_sm > ctas_per_sm) per_sm = ctas_per_sm;
-  if (ctx->claim_mode != 2 && (ctx->claim_mode == 1 || P.njobs <= 4) && per_sm <= 2 &&
-      items > (long long)ctx->sms * 4) {
+  if (ctx->claim_mode != 2 && (ctx->claim_mode == 1 || (P.njobs <= 4 && !P.warp_claim)) &&
+      per_sm <= 2 && items > (long long)ctx->sms * 4) {
     // one CTA per SM, per_sm warps per sub-partition, adjacent strips paired
     const int threads = 128 * per_sm;
     int fit = 0;
@@ -444,6 +444,10 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
       J.map_cdir = r.map_cdir;
       J.bound_offset = (int32_t)std::max<long long>(std::min<long long>(r.bound_offset, 1LL << 29),
                                                     -(1LL << 29));
+      J.rmap_fwd = r.rmap_fwd;
+      J.rmap_rev = r.rmap_rev;
+      J.range_offset = (int32_t)std::max<long long>(std::min<long long>(r.range_offset, 1LL << 29),
+                                                    -(1LL << 29));
       J.nstrips = r.nstrips;
       J.want_final = r.want_final ? 1 : 0;
       J.item_base = item;
@@ -471,7 +475,7 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     }
     // strip-major claim order across jobs (item_job in swb_kernels.cuh)
     int2* d_map = nullptr;
-    if (nj > 1 && !ctx->job_major) {
+    if (nj > 1 && !ctx->job_major) {  // (group-mode launches drop it, see launch_any)
       d_map = A.take<int2>(total_strips);
       long long q = 0;
       int max_strips = 0;
@@ -509,6 +513,10 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     P.proto = ctx->proto;
     P.key_mul = 32;
     P.item_map = d_map;
+    // passes restricted to a narrow corridor are chains along the diagonal:
+    // spread their strips over warps and interleave the jobs (no pairing)
+    for (size_t t = g0; t < g1; ++t)
+      if (reqs[order[t]].rmap_fwd) P.warp_claim = 1;
     memcpy(P.tlo, sc.tlo, sizeof(P.tlo));
     memcpy(P.thi, sc.thi, sizeof(P.thi));
 
@@ -661,6 +669,7 @@ extern "C" int64_t swb_get_option(swb_ctx* ctx, const char* name) {
   if (!strcmp(name, "x2")) return ctx->x2_enabled;
   if (!strcmp(name, "job_major")) return ctx->job_major;
   if (!strcmp(name, "bound_maps")) return ctx->bmaps_on;
+  if (!strcmp(name, "mm_R")) return ctx->mm_R;
   if (!strcmp(name, "mm_prune")) return ctx->mm_prune;
   if (!strcmp(name, "claim_mode")) return ctx->claim_mode;
   if (!strcmp(name, "proto")) return ctx->proto;
@@ -688,6 +697,10 @@ extern "C" int32_t swb_set_option(swb_ctx* ctx, const char* name, int64_t value)
   }
   if (!strcmp(name, "bound_maps")) {
     ctx->bmaps_on = (int)value;
+    return SWB_OK;
+  }
+  if (!strcmp(name, "mm_R")) {
+    ctx->mm_R = (int)value;  // rows per lane of range-limited Myers-Miller passes (0: auto)
     return SWB_OK;
   }
   if (!strcmp(name, "mm_prune")) {

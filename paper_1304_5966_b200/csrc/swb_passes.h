@@ -38,6 +38,9 @@ struct PassReq {
   const int32_t* bmap_in = nullptr;
   int map_nr = 0, map_nc = 0, map_r0 = 0, map_rdir = 1, map_c0 = 0, map_cdir = 1;
   long long bound_offset = 0;
+  const int32_t* rmap_fwd = nullptr;  // static strip ranges (swb_kernels.cuh static_range)
+  const int32_t* rmap_rev = nullptr;
+  long long range_offset = 0;
   // filled by swb_run_passes
   int R = 0;
   bool x2 = false;  // packed 16x2 phase-1 kernel

@@ -17,6 +17,7 @@ ctx = get_context(0)
 
 def timeline(tag):
     t = ctx.debug_times().astype(np.float64)
+    np.save(ROOT / "gpurun_out" / (tag.replace(" ", "_").replace("=", "") + ".npy"), t)
     t0n = t[:, 0].min()
     st, en, wt = (t[:, 0] - t0n) / 1e6, (t[:, 1] - t0n) / 1e6, t[:, 2] / 1e6
     act = en - st
@@ -36,7 +37,7 @@ with Session(ctx, a, b, sc) as S:
     print(f"phase 2 {time.perf_counter() - t0:.3f} s", flush=True)
     timeline("phase2")
     root = phase3._as_array([phase3.Subproblem(start, e, scored.score)], True)
-    for R in (0, 8, 16, 32):
+    for R in [int(x) for x in sys.argv[2:]] or (0, 8, 16, 32):
         ctx.set_option("rows_per_lane", R)
         t0 = time.perf_counter()
         res, cells = ctx.crossings(S.cs, S.s1, S.s2, root, True)
