@@ -205,6 +205,10 @@ int32_t swb_pass(swb_ctx* ctx, const swb_scheme* scheme, const swb_pass_desc* de
  * (seq1, seq2): ceil(n1/1024) x ceil(n2/1024) int32 each.  One pair at a time
  * per context; a later call for another pair replaces them. */
 int32_t swb_bounds_reset(swb_ctx* ctx, int32_t seq1, int32_t seq2);
+/* Diagnostics: copy the forward (which = 1) or reverse (2) map, row-major
+ * nr x nc, raw encoding (value + 2^30, -1 = never written) into out[0..cap);
+ * returns nr * nc (the size when out is NULL). */
+int64_t swb_bounds_read(swb_ctx* ctx, int32_t which, int32_t* out, int64_t cap);
 
 /* --- Myers-Miller level --------------------------------------------------------
  * For each subproblem (rows >= 2 required): run the upper forward and the

@@ -84,6 +84,9 @@ struct JobDev {
   int32_t range_offset;    // static ranges: tile useful iff fwd + rev + range_offset >= target
   const int32_t* rmap_fwd; // static strip ranges from both maps (null: band only)
   const int32_t* rmap_rev;
+  int2* alive;             // per strip (live lo + 1, live hi + 1), 0 = unset (restricted passes)
+  int32_t live_mode;       // bit 0: late start, bit 1: early exit
+  int32_t pad4;
 };
 
 struct PassParams {
@@ -247,6 +250,17 @@ __device__ __forceinline__ void bw_add(const JobDev& J, BoundWriter& w, int ta, 
     else if (w.t0 < 0) { w.t0 = t; w.v0 = v; }
     else { w.t1 = t; w.v1 = v; }
   }
+}
+
+// Mark tiles a strip skips entirely (live-range late start / early exit) as
+// covered by fill: the same bound the skipped fill blocks would have written.
+__device__ __forceinline__ void bw_fill_cols(const JobDev& J, int rt_lo, int rt_hi, int ca, int cb,
+                                             int lane) {
+  if (ca > cb) return;
+  int ta, tb;
+  tile_range(J.map_c0, J.map_cdir, ca, cb, J.map_nc, ta, tb);
+  for (int ct = ta + lane; ct <= tb; ct += 32)
+    for (int rt = rt_lo; rt <= rt_hi; ++rt) atomicMax(J.bmap_out + (long long)rt * J.map_nc + ct, 0);
 }
 
 __device__ __forceinline__ void bw_finish(const JobDev& J, BoundWriter& w, int lane) {
@@ -432,8 +446,49 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     my_progress = J.ext_out_prog;
   }
 
+  // Live column range of a restricted pass.  Its left border
+  // is -inf below row 0, so a strip's cells stay fill until the first live
+  // output of its producer: the strip starts there instead of walking the
+  // fill, and leaves as soon as it is back in fill state with no live input
+  // ahead.  The producer's outputs outside [alo_p, ahi_p) are fill.
+  const bool dyn = J.alive != nullptr && !ext_in && !ext_out;
+  int alo_p = 0, ahi_p = 0x7fffffff;
+  bool lo_set = false;
+  if (dyn && first) ahi_p = 0;  // the restricted top border is -inf
+  if (dyn && (J.live_mode & 1) && s > 0 && cb < ce) {
+    // The producer stores its live lo before the progress release that covers
+    // it and its live hi before its final release, so "no live output" is only
+    // concluded after acquiring the final progress.
+    unsigned ns = 32;
+    for (;;) {
+      const int p = ld_acquire(up_progress);
+      const int ax = ld_relaxed(&J.alive[s - 1].x);
+      if (ax > 0) {
+        alo_p = ax - 1;
+        break;
+      }
+      if (p >= cep) {
+        const int ay = ld_relaxed(&J.alive[s - 1].y);
+        alo_p = 0x7fffffff;
+        if (ay > 0) ahi_p = ay - 1;
+        break;
+      }
+      __nanosleep(ns);
+      ns = ns < 4096 ? ns * 2 : 4096;
+    }
+    const int cb0 = cb;
+    if (alo_p >= ahi_p || alo_p >= ce) cb = ce;
+    else if (alo_p > cb) cb = alo_p;
+    if (J.bmap_out && cb > cb0) {
+      int rl, rh;
+      tile_range(J.map_r0, J.map_rdir, R0, (R0 + 32 * R < n1 ? R0 + 32 * R : n1) - 1, J.map_nr, rl, rh);
+      bw_fill_cols(J, rl, rh, cb0, cb - 1, lane);
+    }
+  }
+
   if (cb >= ce) {
     if (lane == 0) {
+      if (dyn) J.alive[s].y = cb + 1;  // no live output
       if (ext_out) st_release_sys(my_progress, 0x7fffffff);
       else st_release(my_progress, 0x7fffffff);
       J.strip_res[s] = make_int4(0, -1, -1, 0);
@@ -475,7 +530,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     diag = fillm;
   } else if (first) {
     diag = top_h(J.border, cb, go, ge) - goe;
-  } else if (cb - 1 >= cbp && cb - 1 < cep) {
+  } else if (cb - 1 >= cbp && cb - 1 < cep && cb - 1 >= alo_p && cb - 1 < ahi_p) {
     wait_progress(up_progress, cb, ext_in);
     if (ext_in) (void)ld_acquire_sys(up_progress);
     else fence_acq_rel();
@@ -579,7 +634,17 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     }
   };
 
+  bool prev_skipped = false, exited = false;
+  int known_prog2 = 0;  // progress of strip s-2 (previous writer of our buffer)
   for (int s0 = cb; s0 < s_end; s0 += 32) {
+    // early exit (restricted passes): fill state and no live input at or
+    // after column s0 - 1 (lane 0's next diagonal): every later cell is fill
+    if (dyn && (J.live_mode & 2) && prev_skipped && ahi_p < s0) {
+      exited = true;
+      if (lane == 0) J.alive[s].y = (s0 - 31 > cb ? s0 - 31 : cb) + 1;
+      if (J.bmap_out) bw_fill_cols(J, bw.rt_lo, bw.rt_hi, s0 - 31 > cb ? s0 - 31 : cb, ce - 1, lane);
+      break;
+    }
     // (1) stage lane-0 inputs and profile words for columns [s0, s0 + 32).
     // The column codes were prefetched one block ahead; the producer's
     // progress is polled only when the last observed value does not cover
@@ -605,6 +670,10 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
             wait_cycles += clock64() - tw;
           }
           known_prog = ext_in ? ld_acquire_sys(up_progress) : ld_acquire(up_progress);
+          if (dyn && ahi_p == 0x7fffffff) {
+            const int ay = ld_relaxed(&J.alive[s - 1].y);
+            if (ay > 0) ahi_p = ay - 1;
+          }
         }
       }
       if (c < ce) {
@@ -612,7 +681,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
         if (first) {
           th = top_h(J.border, c + 1, go, ge) - goe;
           tf = SWB_NEG32;
-        } else if (c >= cbp && c < cep) {
+        } else if (c >= cbp && c < cep && c >= alo_p && c < ahi_p) {
           int2 v = __ldcg(inbuf + c);
           th = v.x;
           tf = v.y;
@@ -744,10 +813,32 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       __syncwarp();
     }
 
+    prev_skipped = skip;
+
     // (4) flush lane-31 outputs for columns [s0 - 31, s0 + 1) and publish.
     {
       const int c = s0 - 31 + lane;
+      // Buffer s & 1 was written by strip s-2.  Strip s-1 normally consumed
+      // those columns before we could compute them, but a strip that skips
+      // columns (empty or narrowed range, late start, early exit) does not,
+      // so make sure strip s-2 is done with them before overwriting.
+      if (s >= 2 && !ext_out) {
+        const int hi = s0 + 1 < ce ? s0 + 1 : ce;
+        if (hi > cb && known_prog2 < hi) {
+          if (ld_relaxed(J.progress + (s - 2)) < hi) wait_progress(J.progress + (s - 2), hi);
+          known_prog2 = ld_acquire(J.progress + (s - 2));
+        }
+      }
       if (c >= cb && c < ce) __stcg(outbuf + c, sm->out[lane]);
+      if (dyn && !lo_set) {
+        // first live output: consumers start there (ordered by the release below)
+        const unsigned m = __ballot_sync(0xffffffffu, c >= cb && c < ce &&
+                                                          sm->out[lane].x > -(1 << 29));
+        if (m) {
+          lo_set = true;
+          if (lane == 0) J.alive[s].x = s0 - 31 + __ffs(m);  // (lo + 1)
+        }
+      }
       if (ext_out) __threadfence_system();
       else if (P.proto == 0) __threadfence();
       else if (P.proto == 1) fence_acq_rel();
@@ -769,9 +860,11 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     }
   }
   if (J.bmap_out) bw_finish(J, bw, lane);
+  // done: consumers need columns < their own end, strip s+2 needs "finished"
   if (lane == 0) {
-    if (ext_out) st_release_sys(my_progress, ce);
-    else st_release(my_progress, ce);
+    if (dyn && !exited) J.alive[s].y = ce + 1;
+    if (ext_out) st_release_sys(my_progress, 0x7fffffff);
+    else st_release(my_progress, 0x7fffffff);
   }
 
   // Strip result: decode the key, then warp reduction with the mode's tie
@@ -818,7 +911,9 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
     J.strip_times[3 * s + 0] = g0;
     J.strip_times[3 * s + 1] = g1;
-    J.strip_times[3 * s + 2] = gw;
+    // proto 9 (diagnostics): the strip's final column range instead of the wait time
+    J.strip_times[3 * s + 2] =
+        P.proto == 9 ? (((unsigned long long)(unsigned)cb << 32) | (unsigned)ce) : gw;
   }
 }
 

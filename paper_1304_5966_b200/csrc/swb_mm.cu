@@ -424,12 +424,14 @@ extern "C" int32_t swb_crossings(swb_ctx* ctx, const swb_scheme* scheme, int32_t
     if (maps && s.use_bounds) {
       // upper half: a cell c can be on an optimal S->T path only if
       //   U(c) + R'(c) - suffix(T) + slack >= expected   (R' = phase-2 map)
-      swb_bind_maps(ctx, &up, s.si, midr, false, s.sj, cols, false, 0, 2, slack - s.suffix);
+      swb_bind_maps(ctx, &up, s.si, midr, false, s.sj, cols, false, 0, ctx->mm_dyn ? 2 : 0,
+                    slack - s.suffix);
       // lower half: L(c) + H_fwd(c) - prefix(S) + slack >= expected (phase-1 map)
-      swb_bind_maps(ctx, &dn, s.si + midr, rows - midr, true, s.sj, cols, true, 0, 1,
-                    slack - s.prefix);
+      swb_bind_maps(ctx, &dn, s.si + midr, rows - midr, true, s.sj, cols, true, 0,
+                    ctx->mm_dyn ? 1 : 0, slack - s.prefix);
       // static strip ranges: a tile can hold an optimal S->T cell only if
       //   Hf(tile) + R'(tile) + slack - prefix(S) - suffix(T) >= expected
+      if (ctx->mm_static)
       for (PassReq* q : {&up, &dn}) {
         q->rmap_fwd = reinterpret_cast<const int32_t*>(ctx->bmap_fwd.p);
         q->rmap_rev = reinterpret_cast<const int32_t*>(ctx->bmap_rev.p);

@@ -375,6 +375,7 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
       if (r.want_final && r.fin_h_dev == nullptr) final_cols += r.n2;
     }
     size_t bytes = 256 * 8 + sizeof(JobDev) * nj + sizeof(int32_t) * total_strips +
+                   sizeof(int2) * total_strips + 256 +
                    sizeof(unsigned long long) * 5 * nj + sizeof(int32_t) * nj + 64 +
                    sizeof(int4) * total_strips + 24 * total_strips + sizeof(int2) * 2 * total_cols +
                    sizeof(int32_t) * 2 * final_cols + 4096 + 256 * 8 * (size_t)nj +
@@ -389,6 +390,7 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     unsigned long long* d_cnt = A.take<unsigned long long>(5 * nj);
     int32_t* d_pbest = A.take<int32_t>(nj);
     unsigned long long* d_claim = A.take<unsigned long long>(1);
+    int2* d_alive = A.take<int2>(total_strips);  // live ranges (restricted passes)
     size_t zero_end = A.off;
     int4* d_res = A.take<int4>(total_strips);
     unsigned long long* d_times = A.take<unsigned long long>(3 * total_strips);
@@ -444,6 +446,9 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
       J.map_cdir = r.map_cdir;
       J.bound_offset = (int32_t)std::max<long long>(std::min<long long>(r.bound_offset, 1LL << 29),
                                                     -(1LL << 29));
+      J.alive = (r.border == SWB_BORDER_RESTRICTED && !r.ext_in && !r.ext_out && ctx->live_ranges)
+                    ? d_alive + strip_off : nullptr;
+      J.live_mode = ctx->live_ranges;
       J.rmap_fwd = r.rmap_fwd;
       J.rmap_rev = r.rmap_rev;
       J.range_offset = (int32_t)std::max<long long>(std::min<long long>(r.range_offset, 1LL << 29),
@@ -662,6 +667,19 @@ extern "C" int32_t swb_bounds_reset(swb_ctx* ctx, int32_t seq1, int32_t seq2) {
   SWB_API_END();
 }
 
+extern "C" int64_t swb_bounds_read(swb_ctx* ctx, int32_t which, int32_t* out, int64_t cap) {
+  if (!ctx) return -1;
+  const long long n = (long long)ctx->bmap_nr * ctx->bmap_nc;
+  if (!out || cap <= 0) return n;
+  const swb_buf& b = which == 2 ? ctx->bmap_rev : ctx->bmap_fwd;
+  if (!b.p) return 0;
+  cudaStreamSynchronize(ctx->stream);
+  if (cudaMemcpy(out, b.p, sizeof(int32_t) * (size_t)std::min<long long>(n, cap),
+                 cudaMemcpyDeviceToHost) != cudaSuccess)
+    return -1;
+  return n;
+}
+
 extern "C" int64_t swb_get_option(swb_ctx* ctx, const char* name) {
   if (!ctx || !name) return -1;
   if (!strcmp(name, "max_ctas_per_sm")) return ctx->max_ctas_per_sm;
@@ -670,6 +688,10 @@ extern "C" int64_t swb_get_option(swb_ctx* ctx, const char* name) {
   if (!strcmp(name, "job_major")) return ctx->job_major;
   if (!strcmp(name, "bound_maps")) return ctx->bmaps_on;
   if (!strcmp(name, "mm_R")) return ctx->mm_R;
+  if (!strcmp(name, "mm_static")) return ctx->mm_static;
+  if (!strcmp(name, "mm_dyn")) return ctx->mm_dyn;
+  if (!strcmp(name, "live_ranges")) return ctx->live_ranges;
+  if (!strcmp(name, "p2_R")) return ctx->p2_R;
   if (!strcmp(name, "mm_prune")) return ctx->mm_prune;
   if (!strcmp(name, "claim_mode")) return ctx->claim_mode;
   if (!strcmp(name, "proto")) return ctx->proto;
@@ -697,6 +719,22 @@ extern "C" int32_t swb_set_option(swb_ctx* ctx, const char* name, int64_t value)
   }
   if (!strcmp(name, "bound_maps")) {
     ctx->bmaps_on = (int)value;
+    return SWB_OK;
+  }
+  if (!strcmp(name, "mm_dyn")) {
+    ctx->mm_dyn = (int)value;
+    return SWB_OK;
+  }
+  if (!strcmp(name, "mm_static")) {
+    ctx->mm_static = (int)value;
+    return SWB_OK;
+  }
+  if (!strcmp(name, "p2_R")) {
+    ctx->p2_R = (int)value;
+    return SWB_OK;
+  }
+  if (!strcmp(name, "live_ranges")) {
+    ctx->live_ranges = (int)value;
     return SWB_OK;
   }
   if (!strcmp(name, "mm_R")) {
@@ -792,6 +830,8 @@ extern "C" int32_t swb_pass(swb_ctx* ctx, const swb_scheme* scheme, const swb_pa
         return swb_fail(SWB_EINVAL, "bound_read needs a target (prune kind 2 or 3)");
       swb_bind_maps(ctx, &r, d.off1, d.len1, d.rev1 != 0, d.off2, d.len2, d.rev2 != 0,
                     d.bound_write, d.bound_read, d.bound_offset);
+      // a bound-pruned restricted pass is a chain along the path: short strips
+      if (d.bound_read && !r.local && !r.force_R && ctx->p2_R) r.force_R = ctx->p2_R;
     }
   }
   double ms = 0.0;

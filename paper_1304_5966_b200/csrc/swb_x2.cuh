@@ -435,8 +435,8 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
   }
   if (J.bmap_out) bw_finish(J, bw, lane);
   if (lane == 0) {
-    if (ext_out) st_release_sys(my_progress, n2);
-    else st_release(my_progress, n2);
+    if (ext_out) st_release_sys(my_progress, 0x7fffffff);
+    else st_release(my_progress, 0x7fffffff);
   }
 
   // item result: best of both halves, then warp reduction (smallest (i, j) on ties)

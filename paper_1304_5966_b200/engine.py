@@ -127,6 +127,14 @@ class DeviceContext:
     def set_option(self, name: str, value: int) -> None:
         _lib.check(self.lib.swb_set_option(self.ptr, name.encode(), int(value)), "swb_set_option")
 
+    def bounds_map(self, which: int) -> np.ndarray:
+        """Raw tile bound map (1 forward, 2 reverse) of the current pair."""
+        n = int(self.lib.swb_bounds_read(self.ptr, which, None, 0))
+        out = np.zeros(max(n, 0), dtype=np.int32)
+        if n > 0:
+            self.lib.swb_bounds_read(self.ptr, which, out.ctypes.data, n)
+        return out
+
     def get_option(self, name: str) -> int:
         return int(self.lib.swb_get_option(self.ptr, name.encode()))
 
