@@ -18,6 +18,10 @@ score pass with endpoint (score_only).  A step is one full score pass.
             restatement of the reference engine) on a bounded window of the
             same pair, all host threads.
 
+  align_e2e  end-to-end full alignments through `align` (host buffers, phases
+            1-3): C1 10 kbp on the GPU and on the CPU port with a byte-equality
+            check, C3 5 Mbp on the GPU (CPU time extrapolated, lower bound).
+
 `--impl reference` times that CPU port alone on the same metric (rank 0 only).
 Multi-GPU (torchrun, N>1): ONE alignment of an (N x 1 Mbp) x 1 Mbp pair split
 into row slabs, one per GPU, the slab boundary rows streamed GPU to GPU over
@@ -153,6 +157,51 @@ def cpu_window(a, b, target_s: float = 15.0):
     return {"value": w * w / dt / 1e9, "unit": "GCUPS", "cores": threads, "kind": "port",
             "sample": f"score pass on the first {w} x {w} residues of the same pair "
                       f"({dt:.1f} s, score {score})"}, w, dt
+
+
+def align_e2e(swb, scheme, cpu_gcups, with_cpu: bool):
+    """End-to-end alignment time through the public API (`align`, host
+    buffers, phases 1-3), BASELINE configs C1 and C3.  C1 is also run on the
+    CPU port of the reference (oracle/, all host threads) and compared
+    byte-for-byte; C3 on the CPU is extrapolated from the measured CPU score-pass
+    rate (a lower bound: phase 1 alone)."""
+    out = {}
+    a, b = synthetic_pair(10_000, seed=1001)
+    s1 = swb.Sequence.from_codes("target", a, scheme.alphabet)
+    s2 = swb.Sequence.from_codes("query", b, scheme.alphabet)
+    swb.align(s1, s2, scheme)
+    ts = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        summ, path = swb.align(s1, s2, scheme)
+        ts.append(time.perf_counter() - t0)
+    c1 = {"pair": "10 kbp x 10 kbp, mutate 10%, seed 1001", "gpu_s": min(ts), "score": summ.score,
+          "start": list(summ.start), "end": list(summ.end)}
+    if with_cpu:
+        import oracle
+        from oracle.pipeline import max_threads
+        osch = oracle.OracleScheme.match_mismatch(4, 1, -3, 5, 2)
+        t0 = time.perf_counter()
+        ref = oracle.align(a, b, osch, threads=max_threads())
+        c1.update(cpu_s=time.perf_counter() - t0, cpu_cores=max_threads(), cpu_kind="port",
+                  identical=bool(ref[0] == summ.score and tuple(ref[1]) == tuple(summ.start)
+                                 and tuple(ref[2]) == tuple(summ.end)
+                                 and np.array_equal(ref[3], path.ops)))
+    out["C1"] = c1
+    a, b = synthetic_pair(5_000_000, seed=1003)
+    s1 = swb.Sequence.from_codes("target", a, scheme.alphabet)
+    s2 = swb.Sequence.from_codes("query", b, scheme.alphabet)
+    rep = {}
+    t0 = time.perf_counter()
+    summ, path = swb.align(s1, s2, scheme, report=rep)
+    dt = time.perf_counter() - t0
+    c3 = {"pair": "5 Mbp x 5 Mbp, mutate 10%, seed 1003", "gpu_s": dt,
+          "phase_s": [round(x, 3) for x in rep.get("phase_seconds", [])], "score": summ.score,
+          "start": list(summ.start), "end": list(summ.end), "path_ops": int(path.ops.size)}
+    if cpu_gcups:
+        c3["cpu_s_extrapolated_lower_bound"] = a.size * b.size / (cpu_gcups * 1e9)
+    out["C3"] = c3
+    return out
 
 
 def run_reference(args, rank, world):
@@ -294,6 +343,8 @@ def main():
     ap.add_argument("--unrelated", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-align", action="store_true",
+                    help="skip the end-to-end alignment section (C1 vs CPU port, C3)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "native" else args.warmup
 
@@ -402,6 +453,9 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu, _, _ = cpu_window(a, b, target_s=args.cpu_seconds)
+    align = None
+    if rank == 0 and world == 1 and not args.no_align:
+        align = align_e2e(swb, scheme, cpu["value"] if cpu else None, not args.no_cpu)
 
     if rank == 0:
         line = {
@@ -423,6 +477,7 @@ def main():
             "clocks": clocks.summary(),
             "roofline": roofline,
             "cpu_baseline": cpu,
+            "align_e2e": align,
             "int_peak": {k: v for k, v in peak.items() if k != "ms_last"},
         }
         print(json.dumps(line), flush=True)
