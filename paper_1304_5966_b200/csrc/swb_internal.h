@@ -59,7 +59,7 @@ struct swb_ctx {
   int mm_R = 8;
   int mm_static = 1;
   int mm_dyn = 1;               // per-block tile-bound skipping in Myers-Miller halves            // static strip ranges for Myers-Miller halves                 // rows per lane of range-limited Myers-Miller passes
-  swb_buf bmap_fwd, bmap_rev;
+  swb_buf bmap_fwd, bmap_rev, bmap_live;
   // scratch
   swb_buf jobs, rowbuf, progress, results, finals, misc, host_pinned, flush;
   cudaEvent_t tev0 = nullptr, tev1 = nullptr;

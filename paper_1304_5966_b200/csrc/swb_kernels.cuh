@@ -87,6 +87,10 @@ struct JobDev {
   int2* alive;             // per strip (live lo + 1, live hi + 1), 0 = unset (restricted passes)
   int32_t live_mode;       // bit 0: late start, bit 1: early exit
   int32_t pad4;
+  int4* bmap_live;         // writer: per row tile (-(lo+1), hi, covered) of the columns it swept
+  const int4* rmap_live;   // reader: unwritten reverse-map tiles outside that interval are fill
+  int32_t bin_rev;         // bmap_in is the reverse map (rmap_live applies to it)
+  int32_t pad5;
 };
 
 struct PassParams {
@@ -252,15 +256,37 @@ __device__ __forceinline__ void bw_add(const JobDev& J, BoundWriter& w, int ta, 
   }
 }
 
-// Mark tiles a strip skips entirely (live-range late start / early exit) as
-// covered by fill: the same bound the skipped fill blocks would have written.
-__device__ __forceinline__ void bw_fill_cols(const JobDev& J, int rt_lo, int rt_hi, int ca, int cb,
-                                             int lane) {
-  if (ca > cb) return;
-  int ta, tb;
-  tile_range(J.map_c0, J.map_cdir, ca, cb, J.map_nc, ta, tb);
-  for (int ct = ta + lane; ct <= tb; ct += 32)
-    for (int rt = rt_lo; rt <= rt_hi; ++rt) atomicMax(J.bmap_out + (long long)rt * J.map_nc + ct, 0);
+// A strip with a live column range sweeps only [c_lo, c_hi] (pass columns);
+// record, per row tile, the hull of the forward columns its strips swept so a
+// reader can tell "never written because fill" from "never visited".
+__device__ __forceinline__ void live_record(const JobDev& J, int rt_lo, int rt_hi, int c_lo,
+                                            int c_hi) {
+  for (int rt = rt_lo; rt <= rt_hi; ++rt) {
+    int4* e = J.bmap_live + rt;
+    atomicMax(&e->z, 1);
+    if (c_lo <= c_hi) {
+      int fa = J.map_c0 + J.map_cdir * c_lo, fb = J.map_c0 + J.map_cdir * c_hi;
+      if (fa > fb) {
+        const int t = fa;
+        fa = fb;
+        fb = t;
+      }
+      atomicMax(&e->x, -(fa + 1));
+      atomicMax(&e->y, fb);
+    }
+  }
+}
+
+// Decode one reverse-map tile for a reader: raw -1 is +inf unless the tile
+// lies outside the swept interval of its row tile (then fill).
+__device__ __forceinline__ bool map_unknown(const JobDev& J, int raw, int rt, int ct) {
+  if (raw >= 0) return false;
+  if (!J.rmap_live) return true;
+  const int4 e = J.rmap_live[rt];
+  if (!e.z) return true;
+  const int lo = -e.x - 1, hi = e.y;
+  const int t0 = ct << kTileShift, t1 = t0 + (1 << kTileShift) - 1;
+  return !(t1 < lo || t0 > hi);
 }
 
 __device__ __forceinline__ void bw_finish(const JobDev& J, BoundWriter& w, int lane) {
@@ -288,7 +314,10 @@ __device__ __forceinline__ long long br_get(const JobDev& J, BoundReader& r, int
   if (lane < n) {
     const int rt = r.rt_lo + lane / nct, ct = ta + lane % nct;
     m = __ldcg(J.bmap_in + (long long)rt * J.map_nc + ct);
-    unknown = m < 0;
+    if (m < 0) {
+      unknown = !J.bin_rev || map_unknown(J, m, rt, ct);
+      if (!unknown) m = 0;  // swept fill
+    }
   }
   unknown = __any_sync(0xffffffffu, unknown);
   m = __reduce_max_sync(0xffffffffu, m);
@@ -361,7 +390,9 @@ __device__ __forceinline__ void static_range(const JobDev& J, int s, int& cb, in
     if (ct <= ct_hi) {
       for (int rt = rt_lo; rt <= rt_hi; ++rt) {
         const long long k = (long long)rt * J.map_nc + ct;
-        const int a = __ldcg(J.rmap_fwd + k), b = __ldcg(J.rmap_rev + k);
+        const int a = __ldcg(J.rmap_fwd + k);
+        int b = __ldcg(J.rmap_rev + k);
+        if (b < 0 && !map_unknown(J, b, rt, ct)) b = 0;  // swept fill
         if (a < 0 || b < 0 ||
             (long long)a + b - 2 * kBoundEnc + J.range_offset >= (long long)J.prune_target)
           useful = true;
@@ -476,17 +507,16 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       __nanosleep(ns);
       ns = ns < 4096 ? ns * 2 : 4096;
     }
-    const int cb0 = cb;
     if (alo_p >= ahi_p || alo_p >= ce) cb = ce;
     else if (alo_p > cb) cb = alo_p;
-    if (J.bmap_out && cb > cb0) {
-      int rl, rh;
-      tile_range(J.map_r0, J.map_rdir, R0, (R0 + 32 * R < n1 ? R0 + 32 * R : n1) - 1, J.map_nr, rl, rh);
-      bw_fill_cols(J, rl, rh, cb0, cb - 1, lane);
-    }
   }
 
   if (cb >= ce) {
+    if (dyn && J.bmap_live && J.bmap_out && lane == 0) {
+      int rl, rh;
+      tile_range(J.map_r0, J.map_rdir, R0, (R0 + 32 * R < n1 ? R0 + 32 * R : n1) - 1, J.map_nr, rl, rh);
+      live_record(J, rl, rh, 1, 0);  // covered, nothing swept
+    }
     if (lane == 0) {
       if (dyn) J.alive[s].y = cb + 1;  // no live output
       if (ext_out) st_release_sys(my_progress, 0x7fffffff);
@@ -635,14 +665,15 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
   };
 
   bool prev_skipped = false, exited = false;
+  int exit_col = 0;
   int known_prog2 = 0;  // progress of strip s-2 (previous writer of our buffer)
   for (int s0 = cb; s0 < s_end; s0 += 32) {
     // early exit (restricted passes): fill state and no live input at or
     // after column s0 - 1 (lane 0's next diagonal): every later cell is fill
     if (dyn && (J.live_mode & 2) && prev_skipped && ahi_p < s0) {
       exited = true;
+      exit_col = s0;
       if (lane == 0) J.alive[s].y = (s0 - 31 > cb ? s0 - 31 : cb) + 1;
-      if (J.bmap_out) bw_fill_cols(J, bw.rt_lo, bw.rt_hi, s0 - 31 > cb ? s0 - 31 : cb, ce - 1, lane);
       break;
     }
     // (1) stage lane-0 inputs and profile words for columns [s0, s0 + 32).
@@ -860,6 +891,8 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     }
   }
   if (J.bmap_out) bw_finish(J, bw, lane);
+  if (dyn && J.bmap_live && J.bmap_out && lane == 0)
+    live_record(J, bw.rt_lo, bw.rt_hi, cb, exited ? exit_col - 1 : ce - 1);
   // done: consumers need columns < their own end, strip s+2 needs "finished"
   if (lane == 0) {
     if (dyn && !exited) J.alive[s].y = ce + 1;

@@ -449,6 +449,9 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
       J.alive = (r.border == SWB_BORDER_RESTRICTED && !r.ext_in && !r.ext_out && ctx->live_ranges)
                     ? d_alive + strip_off : nullptr;
       J.live_mode = ctx->live_ranges;
+      J.bmap_live = (J.alive && r.bmap_live) ? r.bmap_live : nullptr;
+      J.rmap_live = r.rmap_live;
+      J.bin_rev = r.bin_rev;
       J.rmap_fwd = r.rmap_fwd;
       J.rmap_rev = r.rmap_rev;
       J.range_offset = (int32_t)std::max<long long>(std::min<long long>(r.range_offset, 1LL << 29),
@@ -644,6 +647,10 @@ void swb_bind_maps(swb_ctx* ctx, PassReq* r, long long off1, long long len1, boo
   r->map_cdir = rev2 ? -1 : 1;
   r->bmap_out = write == 1 ? fwd : (write == 2 ? rev : nullptr);
   r->bmap_in = read == 1 ? fwd : (read == 2 ? rev : nullptr);
+  int4* live = reinterpret_cast<int4*>(ctx->bmap_live.p);
+  if (write == 2) r->bmap_live = live;  // reverse map writers record their swept hull
+  r->rmap_live = live;
+  r->bin_rev = read == 2 ? 1 : 0;
   r->bound_offset = offset;
 }
 
@@ -660,6 +667,15 @@ extern "C" int32_t swb_bounds_reset(swb_ctx* ctx, int32_t seq1, int32_t seq2) {
   if (!f || !r) return swb_fail(SWB_ECUDA, "out of device memory for bound maps (%zu bytes)", 2 * bytes);
   SWB_CUDA(cudaMemsetAsync(f, 0xff, bytes, ctx->stream));  // -1: never written (+inf)
   SWB_CUDA(cudaMemsetAsync(r, 0xff, bytes, ctx->stream));
+  // per row tile sweep hull of the reverse pass: (-(lo+1), hi, covered) = empty
+  int4* lv = (int4*)swb_scratch(ctx->bmap_live, sizeof(int4) * (size_t)nr);
+  if (!lv) return swb_fail(SWB_ECUDA, "out of device memory for bound maps");
+  {
+    std::vector<int4> init((size_t)nr, make_int4(INT32_MIN, -1, 0, 0));
+    SWB_CUDA(cudaMemcpyAsync(lv, init.data(), sizeof(int4) * (size_t)nr, cudaMemcpyHostToDevice,
+                             ctx->stream));
+    SWB_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
   ctx->bmap_seq1 = seq1;
   ctx->bmap_seq2 = seq2;
   ctx->bmap_nr = (int)nr;

@@ -38,6 +38,9 @@ struct PassReq {
   const int32_t* bmap_in = nullptr;
   int map_nr = 0, map_nc = 0, map_r0 = 0, map_rdir = 1, map_c0 = 0, map_cdir = 1;
   long long bound_offset = 0;
+  int4* bmap_live = nullptr;          // live-range sweep hulls per row tile (writer)
+  const int4* rmap_live = nullptr;    // reader side of the same
+  int bin_rev = 0;                    // bmap_in is the reverse map
   const int32_t* rmap_fwd = nullptr;  // static strip ranges (swb_kernels.cuh static_range)
   const int32_t* rmap_rev = nullptr;
   long long range_offset = 0;
