@@ -133,3 +133,42 @@ def test_leaf_predicate_and_splice_order():
     lvl["ei"] = [1, 200, 10]
     lvl["ej"] = [500, 300, 10]
     assert phase3._is_leaf(lvl, 16384).tolist() == [True, False, True]
+
+
+class RecordingCtx(OracleCtx):
+    def __init__(self, *a):
+        super().__init__(*a)
+        self.seen = []
+
+    def crossings(self, cs, s1, s2, subs, band):
+        self.seen.append(subs.copy())
+        return super().crossings(cs, s1, s2, subs, band)
+
+
+@pytest.mark.parametrize("seed", [11, 12, 13])
+def test_prefix_suffix_partition_the_score(seed):
+    """Tile-bound pruning needs, for every Myers-Miller
+    subproblem, the optimal path's score before its start (prefix) and after
+    its end (suffix): prefix + expected + suffix must equal the total at every
+    level, and the leaves' prefixes must be the running sums of their
+    expected scores in path order."""
+    rng = np.random.default_rng(seed)
+    a = random_codes(rng, 900)
+    b = mutate_codes(rng, a, 0.15)
+    scheme = dna_scheme()
+    osch = oracle_scheme(scheme)
+    score, start, end, ops = oracle.align(a, b, osch, leaf_limit=64)
+    S = FakeSession(a, b, scheme)
+    S.ctx = RecordingCtx(a, b, osch)
+    S.bounds = True
+    root = phase3._as_array([phase3.Subproblem(Coord(*start), Coord(*end), score)], True)
+    leaves = phase3.collect_leaves(S, root, 64, True)
+    assert len(S.ctx.seen) >= 3
+    for level in S.ctx.seen:
+        assert (level["use_bounds"] == 1).all()
+        assert (level["prefix"] + level["expected"] + level["suffix"] == score).all()
+    assert (leaves["prefix"] + leaves["expected"] + leaves["suffix"] == score).all()
+    run = np.concatenate(([0], np.cumsum(leaves["expected"])[:-1]))
+    assert np.array_equal(leaves["prefix"], run)
+    path = phase3.reconstruct(S, AlignmentSummary(score, Coord(*start), Coord(*end)), leaf_limit=64)
+    assert np.array_equal(path.ops, ops)
