@@ -726,6 +726,11 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       __syncwarp();
     }
     const bool steady = (s0 - 31 >= cb) && (s0 + 32 <= ce);
+    // A restricted pass may also skip its ramp blocks: lanes that have not
+    // reached cb yet hold -inf state (left border below row 0), so resetting
+    // them to fill changes nothing; other border families keep finite left
+    // states there and prune steady blocks only.
+    const bool prunable = steady || J.border == SWB_BORDER_RESTRICTED;
 
     // (2) pruning: skip the whole 32-step block when no path through it can
     // matter.  kind 1 (phase 1): cannot reach the running best
@@ -742,7 +747,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     // with the band's and pruning's fills it bounds every cell of the block
     // from above once max_sub per column is added
     long long inm = 0;
-    if ((J.prune && steady) || J.bmap_out || (J.bmap_in && steady)) {
+    if ((J.prune && prunable) || J.bmap_out || (J.bmap_in && prunable)) {
       int m = out_hm > diag ? out_hm : diag;
 #pragma unroll
       for (int r = 0; r < R; ++r) m = m > H[r] ? m : H[r];
@@ -753,7 +758,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       m = __reduce_max_sync(0xffffffffu, m);
       inm = (long long)m + goe;
     }
-    if (J.prune && steady) {
+    if (J.prune && prunable) {
       const int rem_r = n1 - R0 + J.rows_after;
       const int rem_c = n2 - (s0 - 31);
       const long long ms = P.max_sub;
@@ -784,7 +789,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     }
     // tile bound maps: skip when even the best continuation
     // the map allows cannot reach the target; record this block's bound
-    if (J.bmap_in && steady && !skip) {
+    if (J.bmap_in && prunable && !skip) {
       int ta, tb;
       tile_range(J.map_c0, J.map_cdir, s0 - 32, s0 + 32, J.map_nc, ta, tb);
       const long long mx = br_get(J, brd, ta, tb, lane);
