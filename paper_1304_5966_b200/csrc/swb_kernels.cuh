@@ -182,12 +182,18 @@ __device__ __forceinline__ int ld_relaxed(const int32_t* p) {
 }
 
 // Spin until *p >= need with exponential back-off: a waiting warp shares its
-// SM sub-partition with a computing one, so it must not steal issue slots.
+// SM sub-partition with a computing one, so it must not steal issue slots;
+// the cap keeps the overshoot small against a producer that publishes every
+// 32 steps (~2 us), which is what a chain along the diagonal waits on.
+#ifndef SWB_WAIT_CAP_NS
+#define SWB_WAIT_CAP_NS 256
+#endif
+constexpr unsigned kWaitCapNs = SWB_WAIT_CAP_NS;
 __device__ __forceinline__ void wait_progress(const int32_t* p, int need, bool sys = false) {
   unsigned ns = 32;
   while ((sys ? ld_relaxed_sys(p) : ld_relaxed(p)) < need) {
     __nanosleep(ns);
-    ns = ns < 4096 ? ns * 2 : 4096;
+    ns = ns < kWaitCapNs ? ns * 2 : kWaitCapNs;
   }
 }
 
@@ -505,7 +511,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
         break;
       }
       __nanosleep(ns);
-      ns = ns < 4096 ? ns * 2 : 4096;
+      ns = ns < kWaitCapNs ? ns * 2 : kWaitCapNs;
     }
     if (alo_p >= ahi_p || alo_p >= ce) cb = ce;
     else if (alo_p > cb) cb = alo_p;
