@@ -589,7 +589,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
   }
 
   int out_hm = fillm, out_f = SWB_NEG32;
-  int known_prog = 0, prune_seen = 0;
+  int known_prog = 0, prune_seen = 0, published = 0;
   int code_next = (cb + lane < ce) ? (int)J.cols[(long long)(cb + lane) * J.cstep] : 0;
   long long pruned_blocks = 0, exec_blocks = 0;
   long long wait_cycles = 0;
@@ -897,8 +897,14 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
 
     // (5) running best for pruning (monotone, never ahead of the truth).
     if (LOCAL && J.prune == 1 && TRACK == kTrackMin) {
+      // publish only improvements and only above what is already known:
+      // one contended atomic per warp and block would cost every warp a
+      // global round trip on the critical path
       const int bm = __reduce_max_sync(0xffffffffu, bkey >> 5);
-      if (lane == 0 && bm > -goe) atomicMax(J.prune_best, bm + goe);
+      if (bm > -goe && bm + goe > published && bm + goe > prune_seen) {
+        published = bm + goe;
+        if (lane == 0) atomicMax(J.prune_best, published);
+      }
     }
   }
   if (J.bmap_out) bw_finish(J, bw, lane);

@@ -178,11 +178,11 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     tile_range(J.map_r0, J.map_rdir, R0, r_hi, J.map_nr, bw.rt_lo, bw.rt_hi);
   }
 
-  int known_prog = 0, prune_seen = 0;
+  int known_prog = 0, prune_seen = 0, published = 0;
   int code_next = (lane < n2) ? (int)J.cols[(long long)lane * J.cstep] : 0;
   long long pruned_blocks = 0, exec_blocks = 0, wait_cycles = 0;
   const long long t_strip0 = clock64();
-  unsigned long long g0, gw = 0;
+  unsigned long long g0, gw = 0, g_diag = 0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
   const int s_end = n2 + 63;
 
@@ -317,6 +317,7 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
                              clamp_rel((long long)top_f - base + kX2Off));
     __syncwarp();
     const bool steady = (s0 >= 63) && (s0 + 32 <= n2);
+    if (P.proto == 10 && g_diag == 0 && s0 + 32 > R0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_diag));
 
     // (2) pruning / tracking decision on the 95-column skewed block
     bool skip = false, track_block = true;
@@ -429,8 +430,14 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
 
     // (5) running best for pruning
     if (J.prune == 1) {
+      // publish only improvements and only above what is already known:
+      // one contended atomic per warp and block would cost every warp a
+      // global round trip on the critical path
       const int bm = __reduce_max_sync(0xffffffffu, vA > vB ? vA : vB);
-      if (lane == 0 && bm > -goe) atomicMax(J.prune_best, bm + goe);
+      if (bm > -goe && bm + goe > published && bm + goe > prune_seen) {
+        published = bm + goe;
+        if (lane == 0) atomicMax(J.prune_best, published);
+      }
     }
   }
   if (J.bmap_out) bw_finish(J, bw, lane);
@@ -483,7 +490,7 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
     J.strip_times[3 * s + 0] = g0;
     J.strip_times[3 * s + 1] = g1;
-    J.strip_times[3 * s + 2] = gw;
+    J.strip_times[3 * s + 2] = P.proto == 10 ? g_diag : gw;  // proto 10: diagonal entry time
   }
 }
 
