@@ -54,12 +54,11 @@ struct swb_ctx {
   int bmap_seq1 = -1, bmap_seq2 = -1;
   int bmap_nr = 0, bmap_nc = 0;
   int bmaps_on = 1;             // option "bound_maps": 0 disables reads and writes
-  int live_ranges = 3;          // restricted passes: bit 0 late start, bit 1 early exit
-  int p2_R = 8;
-  int throttle_ns = 0;          // packed kernel critical-path priority (0 = off)                 // rows per lane of bound-pruned restricted passes (phase 2)
-  int mm_R = 8;
-  int mm_static = 1;
-  int mm_dyn = 1;               // per-block tile-bound skipping in Myers-Miller halves            // static strip ranges for Myers-Miller halves                 // rows per lane of range-limited Myers-Miller passes
+  int live_ranges = 3;  // restricted passes: bit 0 late start, bit 1 early exit
+  int p2_R = 8;         // rows per lane of bound-pruned restricted passes (phase 2)
+  int mm_R = 8;         // rows per lane of range-limited Myers-Miller passes
+  int mm_static = 1;    // static strip ranges for Myers-Miller halves
+  int mm_dyn = 1;       // per-block tile-bound skipping in Myers-Miller halves
   swb_buf bmap_fwd, bmap_rev, bmap_live;
   // scratch
   swb_buf jobs, rowbuf, progress, results, finals, misc, host_pinned, flush;
