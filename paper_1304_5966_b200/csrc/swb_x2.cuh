@@ -160,6 +160,8 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
   // per-block key frame: V_ref per half, 1 - V_ref(rel) and the best's key
   long long vrA = 0, vrB = 0;
   uint32_t nv2 = 0u, kb2 = 0u, bk2 = 0u;
+  uint32_t bmax2 = 0u;   // optimistic blocks: packed maximum of hm over the block
+  int opt_cool = 0;      // candidate blocks to track directly after a hit
   auto set_frame = [&](long long mabs_w) {
     const long long lowv = mabs_w + 95LL * P.max_sub - kX2KeyRoom;
     vrA = vA > lowv ? vA : lowv;
@@ -188,7 +190,8 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
 
   auto step = [&](const int k, const int st, const bool guard, uint32_t (&Hin)[R],
                   uint32_t (&Hout)[R], auto trk_tag) {
-    constexpr bool TRK = decltype(trk_tag)::value;
+    constexpr int MODE = decltype(trk_tag)::value;  // 0 untracked, 1 keys, 2 column max only
+    constexpr bool TRK = MODE == 1;
     const int colA = st - lane, colB = colA - 32;
     const int2 tp = sm->tz[tz_off + k];
     const uint32_t tl = sm->prof[64 - lane + k], th = sm->prof[32 - lane + k];
@@ -210,6 +213,7 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     uint32_t fv = up_f;
     uint32_t hab = up_h;
     uint32_t cm = guard ? 0u : bk2, kp = 0u;
+    uint32_t vmx = 0u, vkp = 0u;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const uint32_t sv = prmt(tl, th, sel[r]);
@@ -223,6 +227,11 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
       d = Hin[r];
       Hout[r] = guard ? ((hm & ~keep) | (Hin[r] & keep)) : hm;
       hab = h2m;
+      if (MODE == 2) {
+        if (r & 1) vmx = vimax3_2(vmx, vkp, hm);
+        else if (r == R - 1) vmx = vimax3_2(vmx, hm, hm);
+        vkp = hm;
+      }
       if (TRK) {
         const uint32_t t = viaddmax_relu_2(hm, nv2, NGE2);  // any c <= 0: max(hm + nv, 0)
         const uint32_t key = (uint32_t)imad((int)t, k32, (int)rk[r]);
@@ -233,6 +242,7 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     }
     out_hm = Hout[R - 1];
     out_f = fv;
+    if (MODE == 2) bmax2 = vimax3_2(bmax2, vmx, vmx);
     if (TRK) {
       bk2 = guard ? vimax3_2(bk2, cm & ~keep, 0u) : cm;
       sm->trk[k][lane] = bk2;
@@ -247,7 +257,8 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     int top_h = -goe, top_f = SWB_NEG32;  // local top border: H = 0, F = -inf
     {
       const int code = code_next;
-      const int pb_now = J.prune == 1 ? ld_relaxed(J.prune_best) : 0;
+      // the running best also decides tracking, so it is kept with pruning off
+      const int pb_now = ld_relaxed(J.prune_best);
       {
         const int cn = c + 32;
         code_next = (cn < n2) ? (int)J.cols[(long long)cn * J.cstep] : 0;
@@ -321,14 +332,16 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
 
     // (2) pruning / tracking decision on the 95-column skewed block
     bool skip = false, track_block = true;
-    if (J.prune == 1 && steady) {
+    if (steady) {
       const long long inm = (long long)mabs_w + goe;
       const long long ms = P.max_sub;
-      const int rem_r = n1 - R0 + J.rows_after;
-      const int rem_c = n2 - (s0 - 63);
-      const long long bound = (inm > 0 ? inm : 0) + ms * (long long)(rem_r < rem_c ? rem_r : rem_c);
-      skip = bound < (long long)prune_seen;
       track_block = (inm > 0 ? inm : 0) + 95LL * ms >= (long long)prune_seen;
+      if (J.prune == 1) {
+        const int rem_r = n1 - R0 + J.rows_after;
+        const int rem_c = n2 - (s0 - 63);
+        const long long bound = (inm > 0 ? inm : 0) + ms * (long long)(rem_r < rem_c ? rem_r : rem_c);
+        skip = bound < (long long)prune_seen;
+      }
     }
 
     if (J.bmap_out) {
@@ -361,9 +374,47 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
       ++exec_blocks;
       const bool trk_on = !steady || track_block;
       if (trk_on) set_frame(mabs_w);
-      using T1 = std::integral_constant<bool, true>;
-      using T0 = std::integral_constant<bool, false>;
-      if (steady && !track_block) {
+      using T1 = std::integral_constant<int, 1>;
+      using T0 = std::integral_constant<int, 0>;
+      using T2 = std::integral_constant<int, 2>;
+      bool tracked_run = true;
+      if (steady && track_block && opt_cool == 0) {
+        // Optimistic: the block can only matter if one of its cells reaches
+        // the running best (a smaller cell is never the endpoint).  Run it
+        // with a packed column max only (0.5 instead of 1.5 ALU per pair) and
+        // re-run it tracked from the saved state if the maximum reaches it.
+        uint32_t Hs[R], Es[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          Hs[r] = H[r];
+          Es[r] = E[r];
+        }
+        const uint32_t diag_s = diag, ohm_s = out_hm, of_s = out_f;
+        bmax2 = 0u;
+#pragma unroll 1
+        for (int k = 0; k < 32; k += 2) {
+          step(k, s0 + k, false, H, H2, T2{});
+          step(k + 1, s0 + k + 1, false, H2, H, T2{});
+        }
+        const int mrel2 = __reduce_max_sync(0xffffffffu, lo16(bmax2) > hi16(bmax2) ? lo16(bmax2)
+                                                                                    : hi16(bmax2));
+        if ((long long)mrel2 + base - kX2Off + goe >= (long long)prune_seen) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            H[r] = Hs[r];
+            E[r] = Es[r];
+          }
+          diag = diag_s;
+          out_hm = ohm_s;
+          out_f = of_s;
+          __syncwarp();
+          opt_cool = 4;
+        } else {
+          tracked_run = false;
+        }
+      }
+      if (!tracked_run) {
+      } else if (steady && !track_block) {
 #pragma unroll 1
         for (int k = 0; k < 32; k += 2) {
           step(k, s0 + k, false, H, H2, T0{});
@@ -383,7 +434,13 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
         }
       }
       __syncwarp();
-      if (trk_on && bk2 != kb2) {
+      // a tracked block that found nothing new lets the next candidate try
+      // the optimistic run again
+      if (steady && track_block && tracked_run) {
+        if (!__all_sync(0xffffffffu, bk2 == kb2)) opt_cool = 4;
+        else if (opt_cool > 0) --opt_cool;
+      }
+      if (trk_on && tracked_run && bk2 != kb2) {
         // a strictly better cell in at least one half: first step reaching it
         auto resolve = [&](bool hiHalf, int key, int colbase, int& v, int& rk_, int& bj,
                            long long vref) {
@@ -428,8 +485,8 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
       }
     }
 
-    // (5) running best for pruning
-    if (J.prune == 1) {
+    // (5) running best (pruning and the tracking decision)
+    {
       // publish only improvements and only above what is already known:
       // one contended atomic per warp and block would cost every warp a
       // global round trip on the critical path
