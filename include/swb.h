@@ -69,12 +69,13 @@ extern "C" {
 typedef struct swb_ctx swb_ctx;
 
 /* ScoringScheme (model.py:129-191) restricted to what the kernels need.
- * sub is k x k row-major, sub[a*k + b] = score of seq1 code a vs seq2 code b.
- * k <= 7 (DNA strict, DNA+N); every sub + gap_open + gap_extend must fit in
- * a signed byte (checked, SWB_EUNSUPPORTED otherwise). */
+ * sub is k x k row-major, sub[a*k + b] = score of seq1 code a vs seq2 code b,
+ * k <= 32.  Alphabets of <= 7 symbols whose sub + gap_open + gap_extend fit a
+ * signed byte use register profiles (PRMT); larger ones (protein, BLOSUM62)
+ * a shared-memory table. */
 typedef struct {
   int32_t k;
-  int32_t sub[64];
+  int32_t sub[1024];
   int32_t gap_open;
   int32_t gap_extend;
   int32_t max_sub;

@@ -27,7 +27,7 @@ c_i32, c_i64, c_p = ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p
 
 
 class Scheme(ctypes.Structure):
-    _fields_ = [("k", c_i32), ("sub", c_i32 * 64), ("gap_open", c_i32), ("gap_extend", c_i32),
+    _fields_ = [("k", c_i32), ("sub", c_i32 * 1024), ("gap_open", c_i32), ("gap_extend", c_i32),
                 ("max_sub", c_i32)]
 
 

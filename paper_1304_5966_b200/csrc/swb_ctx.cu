@@ -111,8 +111,8 @@ void swb_ctx_destroy(swb_ctx* ctx) {
     if (s.fwd) cudaFree(s.fwd);
     if (s.rev) cudaFree(s.rev);
   }
-  swb_buf* bufs[] = {&ctx->jobs, &ctx->rowbuf, &ctx->progress, &ctx->results, &ctx->finals,
-                     &ctx->misc, &ctx->flush};
+  swb_buf* bufs[] = {&ctx->jobs,  &ctx->rowbuf, &ctx->progress, &ctx->results, &ctx->finals,
+                     &ctx->misc,  &ctx->flush,  &ctx->bmap_fwd, &ctx->bmap_rev, &ctx->bmap_live};
   if (ctx->tev0) {
     cudaEventDestroy(ctx->tev0);
     cudaEventDestroy(ctx->tev1);
@@ -133,12 +133,12 @@ int32_t swb_seq_upload(swb_ctx* ctx, const uint8_t* codes, int64_t n, int32_t* s
   if (n >= (int64_t)1 << 31) return swb_fail(SWB_ERANGE, "sequence longer than 2^31-1");
   {
     uint8_t acc = 0;
-    for (int64_t x = 0; x < n; ++x) acc |= (uint8_t)(codes[x] >= 7);
+    for (int64_t x = 0; x < n; ++x) acc |= (uint8_t)(codes[x] >= 32);
     if (acc) {
       int64_t x = 0;
-      while (codes[x] < 7) ++x;
+      while (codes[x] < 32) ++x;
       return swb_fail(SWB_EUNSUPPORTED,
-                      "residue code %d at offset %lld: alphabets of more than 7 symbols are not supported",
+                      "residue code %d at offset %lld: alphabets of more than 32 symbols are not supported",
                       (int)codes[x], (long long)x);
     }
   }

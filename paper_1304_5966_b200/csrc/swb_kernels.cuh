@@ -107,7 +107,8 @@ struct PassParams {
   uint32_t tlo[8], thi[8];  // profile word per column code
   const int2* item_map;     // claim order -> (job, strip); null: job-major by item_base
   int32_t warp_claim;       // 1: per-warp claiming even for few jobs (range-limited passes)
-  int32_t pad3;
+  int32_t big;              // substitution table mode (tab) instead of tlo/thi
+  const int32_t* tab;       // 32 x 33 table, device (big schemes)
 };
 
 // Work item -> (job, strip).  Multi-job launches claim strips strip-major
@@ -440,10 +441,14 @@ struct WarpSmem {
 // the smallest (MIN) / largest (MAX) column of that row (kernels.py:73-84).
 constexpr int kKeyClamp = -(1 << 25);
 
-template <int R, bool LOCAL, int TRACK, bool FINAL>
+// BIG: substitutions from a shared-memory table (alphabets up to 32 codes or
+// scores outside the int8 profile): the ring carries the
+// column code's table row offset and every cell does one LDS instead of PRMT.
+template <int R, bool LOCAL, int TRACK, bool FINAL, bool BIG>
 __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, int s,
                                        WarpSmem* sm, const uint32_t* __restrict__ tlo_s,
                                        const uint32_t* __restrict__ thi_s) {
+  const int* __restrict__ tab_s = reinterpret_cast<const int*>(tlo_s);  // BIG: the table
   const JobDev J = Jg;
   const int lane = threadIdx.x & 31;
   const int goe = P.goe, ge = P.ge;
@@ -545,6 +550,10 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int i = lrow0 + r;
+    if (BIG) {
+      sel[r] = (i < n1) ? (uint32_t)J.rows[(long long)i * J.rstep] : 32u;  // 32: pad, entry 0
+      continue;
+    }
     uint32_t a = (i < n1) ? (uint32_t)J.rows[(long long)i * J.rstep] : (uint32_t)kPadCode;
     sel[r] = a | ((a | 8u) << 4) | ((a | 8u) << 8) | ((a | 8u) << 12);
   }
@@ -621,7 +630,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       int fh = 0, ff = 0;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const int sv = (int)prmt(tl, th, sel[r]);
+        const int sv = BIG ? tab_s[rv.z + (int)sel[r]] : (int)prmt(tl, th, sel[r]);
         const int h2 = LOCAL ? __viaddmax_s32_relu(d, sv, E[r]) : __viaddmax_s32(d, sv, E[r]);
         fv = vmaxadd(fv, -ge, hab);
         const int h2m = h2 - goe;
@@ -726,7 +735,8 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
           th = fillm;
           tf = SWB_NEG32;
         }
-        sm->ring[c & 63] = make_int4(th, tf, (int)tlo_s[code], (int)thi_s[code]);
+        if (BIG) sm->ring[c & 63] = make_int4(th, tf, code * 33, 0);
+        else sm->ring[c & 63] = make_int4(th, tf, (int)tlo_s[code], (int)thi_s[code]);
       }
       prune_seen = pb_now;
       __syncwarp();
@@ -967,15 +977,15 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
   }
 }
 
-template <int R, bool LOCAL, int TRACK>
+template <int R, bool LOCAL, int TRACK, bool BIG>
 __device__ __forceinline__ void run_item(const PassParams& P, long long item, WarpSmem* sm,
                                          const uint32_t* tlo_s, const uint32_t* thi_s) {
   int s = 0;
   const JobDev& J = P.jobs[item_job(P, item, &s)];
   if (J.want_final && s == J.nstrips - 1)
-    run_strip<R, LOCAL, TRACK, true>(P, J, s, sm, tlo_s, thi_s);
+    run_strip<R, LOCAL, TRACK, true, BIG>(P, J, s, sm, tlo_s, thi_s);
   else
-    run_strip<R, LOCAL, TRACK, false>(P, J, s, sm, tlo_s, thi_s);
+    run_strip<R, LOCAL, TRACK, false, BIG>(P, J, s, sm, tlo_s, thi_s);
 }
 
 // Persistent launch.  Two claiming modes:
@@ -987,12 +997,14 @@ __device__ __forceinline__ void run_item(const PassParams& P, long long item, Wa
 //    sub-partition hold ADJACENT strips of the chain: when one waits for its
 //    producer the other (its producer or consumer) gets the issue slots, and
 //    every sub-partition carries the same load.
-template <int R, bool LOCAL, int TRACK>
+template <int R, bool LOCAL, int TRACK, bool BIG = false>
 __global__ void __launch_bounds__(256) pass_kernel(const PassParams P) {
   __shared__ WarpSmem wsm[8];
-  __shared__ uint32_t tlo_s[8], thi_s[8];
+  __shared__ uint32_t tlo_s[BIG ? 32 * 33 : 8], thi_s[8];
   __shared__ long long base_s;
-  if (threadIdx.x < 8) {
+  if (BIG) {
+    for (int x = threadIdx.x; x < 32 * 33; x += blockDim.x) tlo_s[x] = (uint32_t)P.tab[x];
+  } else if (threadIdx.x < 8) {
     tlo_s[threadIdx.x] = P.tlo[threadIdx.x];
     thi_s[threadIdx.x] = P.thi[threadIdx.x];
   }
@@ -1018,7 +1030,7 @@ __global__ void __launch_bounds__(256) pass_kernel(const PassParams P) {
         const long long q = P.total_items - 1 - p;
         item = (warp >> 2) == 0 ? (p <= q ? p : P.total_items) : (p < q ? q : P.total_items);
       }
-      if (item < P.total_items) run_item<R, LOCAL, TRACK>(P, item, sm, tlo_s, thi_s);
+      if (item < P.total_items) run_item<R, LOCAL, TRACK, BIG>(P, item, sm, tlo_s, thi_s);
     }
     return;
   }
@@ -1027,7 +1039,7 @@ __global__ void __launch_bounds__(256) pass_kernel(const PassParams P) {
     if (lane == 0) item = (long long)atomicAdd(P.claim, 1ULL);
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item >= P.total_items) break;
-    run_item<R, LOCAL, TRACK>(P, item, sm, tlo_s, thi_s);
+    run_item<R, LOCAL, TRACK, BIG>(P, item, sm, tlo_s, thi_s);
   }
 }
 

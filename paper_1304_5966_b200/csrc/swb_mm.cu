@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(32) leaf_kernel(const LeafDev* leaves, int32_t
                                                   uint8_t* ops, long long* counts,
                                                   long long* scores, const int32_t* sub_g,
                                                   int k, int go, int ge) {
-  __shared__ int32_t sub[64];
+  __shared__ int32_t sub[1024];
   const int lane = threadIdx.x;
   for (int x = lane; x < k * k; x += 32) sub[x] = sub_g[x];
   __syncwarp();
@@ -504,7 +504,7 @@ extern "C" int32_t swb_leaves(swb_ctx* ctx, const swb_scheme* scheme, int32_t se
     return swb_fail(SWB_EINVAL, "bad sequence id");
   const swb_seq& S1 = ctx->seqs[seq1];
   const swb_seq& S2 = ctx->seqs[seq2];
-  int32_t subv[64];
+  int32_t subv[1024];
   for (int x = 0; x < sc.k * sc.k; ++x) subv[x] = scheme->sub[x];
 
   long long ops_total = 0;
@@ -560,7 +560,7 @@ extern "C" int32_t swb_leaves(swb_ctx* ctx, const swb_scheme* scheme, int32_t se
       ++t1;
     }
     const int nb = t1 - t0;
-    const size_t meta = sizeof(LeafDev) * nb + 2 * sizeof(long long) * nb + 64 * 4 + 1024;
+    const size_t meta = sizeof(LeafDev) * nb + 2 * sizeof(long long) * nb + 1024 * 4 + 1024;
     char* base = (char*)swb_scratch(ctx->jobs, meta);
     int32_t* mats = (int32_t*)swb_scratch(ctx->progress, sizeof(int32_t) * (size_t)mat + 256);
     if (!base || !mats) return swb_fail(SWB_ECUDA, "out of device memory for leaf matrices");
@@ -569,7 +569,8 @@ extern "C" int32_t swb_leaves(swb_ctx* ctx, const swb_scheme* scheme, int32_t se
     long long* d_sc = d_cnt + nb;
     d_sub = (int32_t*)(d_sc + nb);
     SWB_CUDA(cudaMemcpyAsync(d_l, L.data(), sizeof(LeafDev) * nb, cudaMemcpyHostToDevice, ctx->stream));
-    SWB_CUDA(cudaMemcpyAsync(d_sub, subv, sizeof(int32_t) * 64, cudaMemcpyHostToDevice, ctx->stream));
+    SWB_CUDA(cudaMemcpyAsync(d_sub, subv, sizeof(int32_t) * sc.k * sc.k, cudaMemcpyHostToDevice,
+                             ctx->stream));
     leaf_kernel<<<nb, 32, 0, ctx->stream>>>(d_l, mats, d_ops, d_cnt, d_sc, d_sub, sc.k, sc.go, sc.ge);
     ctx->launches++;
     SWB_CUDA(cudaGetLastError());

@@ -28,8 +28,8 @@ __global__ void fill_finals_kernel(const swb::JobDev* __restrict__ jobs, int nj)
 
 int swb_prepare_scheme(const swb_scheme* s, SchemeInt* out) {
   if (!s) return swb_fail(SWB_EINVAL, "null scheme");
-  if (s->k < 1 || s->k > 7)
-    return swb_fail(SWB_EUNSUPPORTED, "alphabet size %d not supported (1..7)", s->k);
+  if (s->k < 1 || s->k > 32)
+    return swb_fail(SWB_EUNSUPPORTED, "alphabet size %d not supported (1..32)", s->k);
   if (s->gap_open < 0 || s->gap_extend < 1)
     return swb_fail(SWB_EINVAL, "gap_open must be >= 0 and gap_extend >= 1");
   const int goe = s->gap_open + s->gap_extend;
@@ -43,17 +43,22 @@ int swb_prepare_scheme(const swb_scheme* s, SchemeInt* out) {
   out->max_sub = mx;
   if (mx != s->max_sub)
     return swb_fail(SWB_EINVAL, "max_sub %d does not match the matrix maximum %d", s->max_sub, mx);
+  // register profiles (PRMT bytes) when they fit, else the shared table
+  out->big = s->k > 7;
+  for (int a = 0; a < s->k && !out->big; ++a)
+    for (int b = 0; b < s->k; ++b) {
+      const int v = s->sub[a * s->k + b] + goe;
+      if (v < -127 || v > 127) out->big = 1;
+    }
+  memset(out->tab, 0, sizeof(out->tab));
+  for (int c = 0; c < s->k; ++c)
+    for (int a = 0; a < s->k; ++a) out->tab[c * kTabStride + a] = s->sub[a * s->k + c] + goe;
+  if (out->big) return SWB_OK;
   for (int b = 0; b < 8; ++b) {
     uint8_t bytes[8];
     for (int a = 0; a < 8; ++a) {
       int v = -128;
-      if (a < s->k && b < s->k) {
-        v = s->sub[a * s->k + b] + goe;
-        if (v < -127 || v > 127)
-          return swb_fail(SWB_EUNSUPPORTED,
-                          "substitution %d + gap_open + gap_extend %d does not fit the int8 profile",
-                          s->sub[a * s->k + b], goe);
-      }
+      if (a < s->k && b < s->k) v = s->sub[a * s->k + b] + goe;
       bytes[a] = (uint8_t)(int8_t)v;
     }
     memcpy(&out->tlo[b], bytes, 4);
@@ -102,10 +107,10 @@ namespace {
 constexpr int kLocalR[] = {8, 16, 20, 24, 28, 32};
 constexpr int kOtherR[] = {2, 8, 16, 24, 32};
 
-template <int R, bool LOCAL, int TRACK>
+template <int R, bool LOCAL, int TRACK, bool BIG = false>
 int kernel_occupancy(int* per_sm) {
-  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, pass_kernel<R, LOCAL, TRACK>,
-                                                            128, 0);
+  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      per_sm, pass_kernel<R, LOCAL, TRACK, BIG>, 128, 0);
 }
 
 template <typename K>
@@ -146,9 +151,40 @@ int launch_any(swb_ctx* ctx, K kern, const PassParams& Pin, long long items, int
   return SWB_OK;
 }
 
-template <int R, bool LOCAL, int TRACK>
+template <int R, bool LOCAL, int TRACK, bool BIG = false>
 int launch_kernel(swb_ctx* ctx, const PassParams& Pin, long long items, int ctas_per_sm) {
-  return launch_any(ctx, pass_kernel<R, LOCAL, TRACK>, Pin, items, ctas_per_sm);
+  return launch_any(ctx, pass_kernel<R, LOCAL, TRACK, BIG>, Pin, items, ctas_per_sm);
+}
+
+// Shared-table kernels (large alphabets): few strip heights.
+constexpr int kBigLocalR[] = {8, 16};
+constexpr int kBigOtherR[] = {8};
+
+template <int R>
+int dispatch_big_R(swb_ctx* ctx, const PassParams* P, long long items, bool local, int track,
+                   int ctas_per_sm, int* occ_out) {
+  if (local) {
+    if (track != kTrackMin) return swb_fail(SWB_EUNSUPPORTED, "local passes support TRACK_MIN only");
+    if (occ_out) return kernel_occupancy<R, true, kTrackMin, true>(occ_out);
+    return launch_kernel<R, true, kTrackMin, true>(ctx, *P, items, ctas_per_sm);
+  }
+  if (track == kTrackNone) {
+    if (occ_out) return kernel_occupancy<R, false, kTrackNone, true>(occ_out);
+    return launch_kernel<R, false, kTrackNone, true>(ctx, *P, items, ctas_per_sm);
+  }
+  if (track == kTrackMin) {
+    if (occ_out) return kernel_occupancy<R, false, kTrackMin, true>(occ_out);
+    return launch_kernel<R, false, kTrackMin, true>(ctx, *P, items, ctas_per_sm);
+  }
+  if (occ_out) return kernel_occupancy<R, false, kTrackMax, true>(occ_out);
+  return launch_kernel<R, false, kTrackMax, true>(ctx, *P, items, ctas_per_sm);
+}
+
+int dispatch_big(swb_ctx* ctx, int R, const PassParams* P, long long items, bool local, int track,
+                 int ctas_per_sm, int* occ_out) {
+  if (R == 8) return dispatch_big_R<8>(ctx, P, items, local, track, ctas_per_sm, occ_out);
+  if (R == 16 && local) return dispatch_big_R<16>(ctx, P, items, local, track, ctas_per_sm, occ_out);
+  return swb_fail(SWB_EINVAL, "rows_per_lane %d not instantiated for large alphabets", R);
 }
 
 // packed 16x2 phase-1 kernel (swb_x2.cuh): R packed rows per lane, 64R rows per item
@@ -232,11 +268,13 @@ struct Shape {
 };
 
 Shape choose_shape(swb_ctx* ctx, const std::vector<PassReq*>& jobs, bool local, int track,
-                   bool x2) {
-  const int* cand = x2 ? kX2R : (local ? kLocalR : kOtherR);
-  const int ncand = x2 ? (int)(sizeof(kX2R) / sizeof(int))
-                       : (local ? (int)(sizeof(kLocalR) / sizeof(int))
-                                : (int)(sizeof(kOtherR) / sizeof(int)));
+                   bool x2, bool big) {
+  const int* cand = x2 ? kX2R : big ? (local ? kBigLocalR : kBigOtherR) : (local ? kLocalR : kOtherR);
+  const int ncand = x2    ? (int)(sizeof(kX2R) / sizeof(int))
+                    : big ? (local ? (int)(sizeof(kBigLocalR) / sizeof(int))
+                                   : (int)(sizeof(kBigOtherR) / sizeof(int)))
+                          : (local ? (int)(sizeof(kLocalR) / sizeof(int))
+                                   : (int)(sizeof(kOtherR) / sizeof(int)));
   const int rows_mul = x2 ? 64 : 32;
   const int smsp = ctx->sms * 4;
   Shape best;
@@ -244,8 +282,9 @@ Shape choose_shape(swb_ctx* ctx, const std::vector<PassReq*>& jobs, bool local, 
   for (int q = 0; q < ncand; ++q) {
     const int R = cand[q];
     int occ = 0;
-    const int rc = x2 ? dispatch_x2(ctx, R, nullptr, 0, 0, &occ)
-                      : dispatch(ctx, R, nullptr, 0, local, track, 0, &occ);
+    const int rc = x2    ? dispatch_x2(ctx, R, nullptr, 0, 0, &occ)
+                   : big ? dispatch_big(ctx, R, nullptr, 0, local, track, 0, &occ)
+                         : dispatch(ctx, R, nullptr, 0, local, track, 0, &occ);
     if (rc != cudaSuccess || occ < 1) continue;
     const long long rows_item = (long long)rows_mul * R;
     long long strips = 0, chain = 0;
@@ -313,7 +352,7 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
   // warp's window (<= 1024 rows + 96 columns, plus 32 columns of growth) lies
   // within kX2Span of the window maximum and the relative frame never clamps one.
   const long long ms = std::max(sc.max_sub, 0);
-  bool x2_scheme = sc.k <= 4 && ctx->x2_enabled && 95 * ms <= 1021 &&
+  bool x2_scheme = sc.k <= 4 && !sc.big && ctx->x2_enabled && 95 * ms <= 1021 &&
                    1120LL * (sc.goe + ms) + 32LL * ms + sc.goe <= 25000;
   for (int b = 0; b < sc.k && x2_scheme; ++b)
     for (int a = 0; a < sc.k; ++a) {
@@ -337,7 +376,7 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     size_t b = a;
     std::vector<PassReq*> js;
     while (b < order.size() && cls(order[b]) == cls(order[a])) js.push_back(&reqs[order[b++]]);
-    Shape sh = choose_shape(ctx, js, js[0]->local, js[0]->track, js[0]->x2);
+    Shape sh = choose_shape(ctx, js, js[0]->local, js[0]->track, js[0]->x2, sc.big != 0);
     if (js[0]->x2 && ctx->x2_R) sh.R = ctx->x2_R;
     if (js[0]->x2)
       for (PassReq* r : js)
@@ -375,7 +414,7 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
       if (r.want_final && r.fin_h_dev == nullptr) final_cols += r.n2;
     }
     size_t bytes = 256 * 8 + sizeof(JobDev) * nj + sizeof(int32_t) * total_strips +
-                   sizeof(int2) * total_strips + 256 +
+                   sizeof(int2) * total_strips + 256 + sizeof(int32_t) * 32 * kTabStride + 256 +
                    sizeof(unsigned long long) * 5 * nj + sizeof(int32_t) * nj + 64 +
                    sizeof(int4) * total_strips + 24 * total_strips + sizeof(int2) * 2 * total_cols +
                    sizeof(int32_t) * 2 * final_cols + 4096 + 256 * 8 * (size_t)nj +
@@ -392,6 +431,7 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     unsigned long long* d_claim = A.take<unsigned long long>(1);
     int2* d_alive = A.take<int2>(total_strips);  // live ranges (restricted passes)
     size_t zero_end = A.off;
+    int32_t* d_tab = sc.big ? A.take<int32_t>(32 * kTabStride) : nullptr;
     int4* d_res = A.take<int4>(total_strips);
     unsigned long long* d_times = A.take<unsigned long long>(3 * total_strips);
     // host staging (pinned)
@@ -495,6 +535,9 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     if (A.off > bytes) return swb_fail(SWB_ECUDA, "internal: pass arena overflow");
 
     SWB_CUDA(cudaMemcpyAsync(d_jobs, h_jobs, sizeof(JobDev) * nj, cudaMemcpyHostToDevice, ctx->stream));
+    if (d_tab)
+      SWB_CUDA(cudaMemcpyAsync(d_tab, sc.tab, sizeof(int32_t) * 32 * kTabStride,
+                               cudaMemcpyHostToDevice, ctx->stream));
     if (d_map)
       SWB_CUDA(cudaMemcpyAsync(d_map, h_map, sizeof(int2) * total_strips, cudaMemcpyHostToDevice,
                                ctx->stream));
@@ -521,6 +564,8 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     P.proto = ctx->proto;
     P.key_mul = 32;
     P.item_map = d_map;
+    P.big = sc.big;
+    P.tab = d_tab;
     // passes restricted to a narrow corridor are chains along the diagonal:
     // spread their strips over warps and interleave the jobs (no pairing)
     for (size_t t = g0; t < g1; ++t)
@@ -531,8 +576,9 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     SWB_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
     int rc;
     int ctas = ctx->max_ctas_per_sm ? ctx->max_ctas_per_sm : cls_ctas[order[g0]];
-    rc = head.x2 ? dispatch_x2(ctx, R, &P, item, ctas, nullptr)
-                 : dispatch(ctx, R, &P, item, head.local, head.track, ctas, nullptr);
+    rc = head.x2  ? dispatch_x2(ctx, R, &P, item, ctas, nullptr)
+         : sc.big ? dispatch_big(ctx, R, &P, item, head.local, head.track, ctas, nullptr)
+                  : dispatch(ctx, R, &P, item, head.local, head.track, ctas, nullptr);
     if (rc) return rc;
     SWB_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
     SWB_CUDA(cudaMemcpyAsync(h_res, d_res, sizeof(int4) * total_strips, cudaMemcpyDeviceToHost,

@@ -5,9 +5,13 @@
 
 #include "swb_internal.h"
 
+constexpr int kTabStride = 33;  // table row per column code: 32 row codes + the pad code
+
 struct SchemeInt {
   int goe, ge, go, max_sub, k;
   uint32_t tlo[8], thi[8];
+  int big = 0;                     // 1: shared-memory table (k > 7 or wide scores)
+  int32_t tab[32 * kTabStride];    // tab[c * 33 + a] = sub(a, c) + go + ge; a = 32: pad (0)
 };
 
 struct PassReq {

@@ -43,8 +43,8 @@ _ctx_lock = threading.Lock()
 
 def scheme_struct(scheme: ScoringScheme) -> _lib.Scheme:
     k = len(scheme.alphabet)
-    if k > 7:
-        raise ValueError(f"alphabets of {k} symbols are not supported on the device (max 7)")
+    if k > 32:
+        raise ValueError(f"alphabets of {k} symbols are not supported on the device (max 32)")
     s = _lib.Scheme()
     s.k = k
     flat = np.asarray(scheme.matrix, dtype=np.int64).reshape(-1)

@@ -34,6 +34,11 @@ def golden_medium():
     return load_golden("golden_medium.json.gz")
 
 
+@pytest.fixture(scope="session")
+def golden_protein():
+    return load_golden("golden_protein.json.gz")
+
+
 @pytest.fixture
 def rng():
     return np.random.default_rng(20240811)

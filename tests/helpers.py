@@ -13,7 +13,8 @@ from paper_1304_5966_b200 import Alphabet, ScoringScheme, Sequence
 
 def golden_inputs(rec):
     sch = rec["scheme"]
-    alpha = Alphabet("nucleotide", sch["symbols"], sch["wildcard"])
+    kind = "nucleotide" if len(sch["symbols"]) <= 5 else "protein"
+    alpha = Alphabet(kind, sch["symbols"], sch["wildcard"])
     scheme = ScoringScheme(alpha, np.array(sch["matrix"], dtype=np.int64), sch["gap_open"],
                            sch["gap_extend"], int(np.max(sch["matrix"])))
     s1 = Sequence.make("a", rec["seq1"], alpha)

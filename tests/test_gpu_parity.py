@@ -145,3 +145,28 @@ def test_engine_facade_final_rows():
         assert np.array_equal(got.final_row_h > -(2 ** 40), fin), border
         fin_f = want.final_f > -(2 ** 40)
         assert np.array_equal(got.final_row_f[fin_f], want.final_f[fin_f]), border
+
+
+def test_golden_protein_blosum62(golden_protein):
+    """24-symbol BLOSUM62 scheme: the shared-table kernels
+    reproduce the reference's score, start, end and CIGAR."""
+    for rec in golden_protein:
+        _check_rec(rec)
+
+
+@pytest.mark.parametrize("seed,n", [(1, 3000), (2, 12_000)])
+def test_protein_vs_oracle(seed, n, golden_protein):
+    s1g, _, scheme = golden_inputs(golden_protein[0])
+    k = len(scheme.alphabet)
+    rng = np.random.default_rng(seed)
+    a = random_codes(rng, n, 20)
+    b = mutate_codes(rng, a, 0.3, 20)
+    osch = oracle_scheme(scheme)
+    want = oracle.align(a, b, osch)
+    s1 = Sequence.from_codes("a", a, scheme.alphabet)
+    s2 = Sequence.from_codes("b", b, scheme.alphabet)
+    summ, path = swb.align(s1, s2, scheme)
+    assert (summ.score, tuple(summ.start), tuple(summ.end)) == (want[0], tuple(want[1]),
+                                                              tuple(want[2]))
+    assert np.array_equal(path.ops, want[3])
+    assert k == 24

@@ -35,6 +35,12 @@ def test_oracle_small_golden(golden_small):
         _check(rec)
 
 
+def test_oracle_protein_golden(golden_protein):
+    # BLOSUM62, 24 symbols (tests/golden/make_golden_protein.py)
+    for rec in golden_protein[:60]:
+        _check(rec)
+
+
 def test_oracle_medium_golden(golden_medium):
     for rec in golden_medium:
         _check(rec, threads=4)
