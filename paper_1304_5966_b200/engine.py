@@ -169,6 +169,28 @@ class DeviceContext:
         return float(self.lib.swb_last_kernel_ms(self.ptr))
 
 
+class AllocationMeter:
+    """engine.AllocationMeter (engine.py:74-90): counts live DP-state elements.
+    The device path reports, per launch, its row buffers and the lane state of
+    its strips (Session.run), so the linear-memory property can be checked the
+    same way as on the reference."""
+
+    def __init__(self):
+        self._lock = threading.Lock()
+        self.current = 0
+        self.peak = 0
+
+    def add(self, n: int):
+        with self._lock:
+            self.current += n
+            if self.current > self.peak:
+                self.peak = self.current
+
+    def release(self, n: int):
+        with self._lock:
+            self.current -= n
+
+
 def bound_slack(scheme: ScoringScheme) -> int:
     """Slack of the tile-bound tests (same formula as swb_crossings): junction
     gaps and the cell counted by both halves of a split path."""
@@ -233,6 +255,7 @@ class Session:
         self.cells = 0
         self.target_prune = True  # phase-2 restricted searches skip hopeless blocks
         self.bounds = False       # tile bound maps filled for this pair (reset_bounds)
+        self.meter = None         # engine.AllocationMeter analogue (state_cells per pass)
 
     def reset_bounds(self) -> None:
         """Clear the pair's tile bound maps; phases 1 and 2 of
@@ -301,7 +324,17 @@ class Session:
                 fin = (np.empty(n2 + 1, dtype=np.int64), np.empty(n2 + 1, dtype=np.int64))
             finals.append(fin)
             descs.append(self.desc(final=fin, **sp))
-        outs = self.ctx.passes(self.cs, descs)
+        # device DP state of the launch, in array elements like the reference's
+        # AllocationMeter (engine.py:197-205): two (H, F) row buffers per pass
+        # plus the per-row lane state (H, E) of the strips in flight
+        cells = sum(4 * (int(d.len2) + 1) + 2 * int(d.len1) for d in descs)
+        if self.meter is not None:
+            self.meter.add(cells)
+        try:
+            outs = self.ctx.passes(self.cs, descs)
+        finally:
+            if self.meter is not None:
+                self.meter.release(cells)
         res = []
         for o, fin in zip(outs, finals):
             self.kernel_ms += o.kernel_ms
@@ -365,6 +398,7 @@ class WavefrontEngine:
         if c1.size < 1 or c2.size < 1:
             raise ValueError("cannot tile an empty matrix")
         with Session(get_context(self.device), c1, c2, spec.scheme) as S:
+            S.meter = self.meter
             return S.run([dict(rows=(0, c1.size, 0), cols=(0, c2.size, 0), border=spec.border,
                                clamp=spec.clamp_zero, track=spec.track, band=spec.band,
                                prune=spec.prune, want_final=spec.want_final_rows)])[0]

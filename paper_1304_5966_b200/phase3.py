@@ -88,7 +88,15 @@ def _is_leaf(level: np.ndarray, leaf_limit: int) -> np.ndarray:
 def _split_level(S: Session, level: np.ndarray, band: bool) -> np.ndarray:
     """Replace every subproblem of `level` by its two children, in order
     (upper child first), via one batched device call."""
-    res, cells = S.ctx.crossings(S.cs, S.s1, S.s2, level, band)
+    meter = getattr(S, "meter", None)
+    state = int((8 * (level["ej"] - level["sj"] + 1) + 2 * (level["ei"] - level["si"])).sum())
+    if meter is not None:  # both halves' row buffers and final rows, lane state
+        meter.add(state)
+    try:
+        res, cells = S.ctx.crossings(S.cs, S.s1, S.s2, level, band)
+    finally:
+        if meter is not None:
+            meter.release(state)
     S.cells += cells
     bad = np.flatnonzero(res["status"])
     if bad.size:

@@ -61,6 +61,7 @@ def align(seq1: Sequence, seq2: Sequence, scheme: ScoringScheme,
         raise ValueError("alignment inputs must be non-empty")
     scheme = validate_scheme(scheme)
     with Session(get_context(cfg.device), seq1.codes, seq2.codes, scheme) as S:
+        S.meter = cfg.meter
         if cfg.split == 2:
             out = split_mod.split_align(S, cfg.leaf_limit, cfg.band, report)
             if report is not None:

@@ -170,3 +170,22 @@ def test_protein_vs_oracle(seed, n, golden_protein):
                                                               tuple(want[2]))
     assert np.array_equal(path.ops, want[3])
     assert k == 24
+
+
+def test_allocation_meter_linear():
+    """engine.AllocationMeter parity (test_engine.py:132-146): the device state
+    a pass reports grows linearly with the sequence lengths."""
+    from paper_1304_5966_b200 import AllocationMeter
+    rng = np.random.default_rng(5)
+    sc = dna_scheme()
+    peaks = {}
+    for n in (2000, 8000, 32000):
+        c = random_codes(rng, n)
+        meter = AllocationMeter()
+        s = Sequence.from_codes("a", c, sc.alphabet)
+        swb.align(s, s, sc, AlignConfig(meter=meter))
+        peaks[n] = meter.peak
+        assert meter.current == 0
+    ratios = [peaks[n] / (2 * n) for n in peaks]
+    assert max(ratios) / min(ratios) < 1.1
+    assert max(ratios) < 16
