@@ -169,6 +169,43 @@ class DeviceContext:
         return float(self.lib.swb_last_kernel_ms(self.ptr))
 
 
+@dataclass(frozen=True)
+class BlockGrid:
+    """engine.BlockGrid (engine.py:34-55): the reference's CPU tiling plan,
+    kept for API parity (the device decomposes into warp strips instead;
+    results do not depend on the tiling, SURVEY.md §0 finding 1)."""
+
+    rows: int
+    cols: int
+    block_rows: int
+    block_cols: int
+    grid_rows: int
+    grid_cols: int
+
+    @property
+    def anti_diagonals(self) -> int:
+        return self.grid_rows + self.grid_cols - 1
+
+    def row_span(self, bi: int) -> tuple[int, int]:
+        r0 = bi * self.block_rows
+        return r0, min(r0 + self.block_rows, self.rows)
+
+    def col_span(self, bj: int) -> tuple[int, int]:
+        c0 = bj * self.block_cols
+        return c0, min(c0 + self.block_cols, self.cols)
+
+
+def plan_grid(len1: int, len2: int, block_rows: int = DEFAULT_BLOCK_ROWS,
+              block_cols: int = DEFAULT_BLOCK_COLS) -> BlockGrid:
+    """engine.plan_grid (engine.py:58-71)."""
+    if len1 < 1 or len2 < 1:
+        raise ValueError("cannot tile an empty matrix")
+    block_rows = max(1, min(block_rows, len1))
+    block_cols = max(1, min(block_cols, len2))
+    return BlockGrid(len1, len2, block_rows, block_cols, -(-len1 // block_rows),
+                     -(-len2 // block_cols))
+
+
 class AllocationMeter:
     """engine.AllocationMeter (engine.py:74-90): counts live DP-state elements.
     The device path reports, per launch, its row buffers and the lane state of

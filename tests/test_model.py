@@ -87,3 +87,14 @@ def test_path_end_and_errors():
     with pytest.raises(ValueError):
         cigar_to_ops("3Q")
     assert set(BUG_ERRORS) == {ScoreMismatch, StartNotFound}
+
+
+def test_plan_grid_matches_reference_tiling():
+    from paper_1304_5966_b200 import plan_grid
+    g = plan_grid(1000, 700, 512, 512)
+    assert (g.grid_rows, g.grid_cols, g.anti_diagonals) == (2, 2, 3)
+    assert g.row_span(1) == (512, 1000) and g.col_span(1) == (512, 700)
+    assert plan_grid(10, 10, 512, 512).block_rows == 10
+    import pytest
+    with pytest.raises(ValueError):
+        plan_grid(0, 5)
