@@ -73,3 +73,31 @@ def test_x2_narrow_after_32bit_launch(n1, n2):
     for _ in range(3):
         ref, x2 = _both(a, b, dna_scheme(), prune=False)[::-1]
         assert x2 == ref == (want[0], want[1]), (x2, ref, want[:2])
+
+
+@pytest.mark.parametrize("n,seed", [(20000, 2), (5000, 4)])
+def test_x2_invariant_to_shape(n, seed):
+    """Every rows-per-lane, launch shape and pruning setting of the packed
+    kernel gives the 32-bit kernel's (score, end)."""
+    rng = np.random.default_rng(seed)
+    a = random_codes(rng, n)
+    b = mutate_codes(rng, a, 0.12)[:n]
+    sc = dna_scheme()
+    ctx = get_context(0)
+    saved = {k: ctx.get_option(k) for k in ("x2", "x2_R", "max_ctas_per_sm")}
+    s1 = Sequence.from_codes("a", a, sc.alphabet)
+    s2 = Sequence.from_codes("b", b, sc.alphabet)
+    res = set()
+    try:
+        for x2, R, ctas in ((0, 0, 0), (1, 8, 0), (1, 10, 0), (1, 12, 0), (1, 14, 0), (1, 16, 0),
+                            (1, 8, 1), (1, 14, 2)):
+            ctx.set_option("x2", x2)
+            ctx.set_option("x2_R", R)
+            ctx.set_option("max_ctas_per_sm", ctas)
+            for prune in (True, False):
+                r = swb.score_only(s1, s2, sc, AlignConfig(prune=prune))
+                res.add((r.score, tuple(r.end)))
+    finally:
+        for k, v in saved.items():
+            ctx.set_option(k, v)
+    assert len(res) == 1, res
