@@ -10,12 +10,13 @@ from helpers import dna_scheme, mutate_codes, oracle_scheme, random_codes
 import paper_1304_5966_b200 as swb
 rng0 = np.random.default_rng(int(sys.argv[1]) if len(sys.argv) > 1 else 1)
 fails = 0
+SIZES = [int(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else [3000, 12000, 40000, 90000]
 t0 = time.time()
 for t in range(int(sys.argv[2]) if len(sys.argv) > 2 else 40):
     rng = np.random.default_rng(rng0.integers(1 << 30))
     args = [(1, -3, 5, 2), (2, -1, 3, 2), (5, -2, 0, 4), (3, -5, 10, 1), (1, -1, 2, 1), (4, -4, 6, 3)][t % 6]
     sc = dna_scheme(None, *args)
-    n = int(rng.choice([3000, 12000, 40000, 90000]))
+    n = int(rng.choice(SIZES))
     kind = t % 4
     a = random_codes(rng, n)
     if kind == 0:
