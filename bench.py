@@ -209,19 +209,20 @@ def run_reference(args, rank, world):
     if rank != 0:
         return 0
     a, b = synthetic_pair(args.n, homologous=not args.unrelated)
-    vals = []
+    vals, secs = [], []
     base = None
     for it in range(args.warmup + args.steps):
         cb, w, dt = cpu_window(a, b, target_s=args.cpu_seconds)
         if it >= args.warmup:
             vals.append(cb["value"])
+            secs.append(dt)
             base = cb
     value = statistics.mean(vals)
     line = {
         "metric": "GCUPS (score pass, full-matrix cells / time)", "value": value, "unit": "GCUPS",
         "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "int64", "data": "synthetic",
+        "ms_per_step": 1e3 * statistics.mean(secs), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": f"C2 window: score pass on a square window of the "
                                f"{args.n} x {args.n} homologous pair", "n1": args.n, "n2": args.n,
                    "scheme": "match +1 / mismatch -3 / gap 5+2k"},
