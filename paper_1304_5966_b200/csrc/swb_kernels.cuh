@@ -786,6 +786,9 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       } else if (J.prune == 2) {
         const long long bound = inm + ms * (long long)(rem_r < rem_c ? rem_r : rem_c);
         skip = bound < (long long)J.prune_target;
+        // the pass maximum equals the target (phase 2): a block none of whose
+        // cells can reach it cannot hold the answer, so it runs untracked
+        track_block = inm + 63LL * ms >= (long long)J.prune_target;
       } else {
         int i_hi = R0 + 32 * R;
         if (i_hi > n1) i_hi = n1;
@@ -854,6 +857,12 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
         for (int k = 0; k < 32; k += 2) {
           step(k, s0 + k, false, H, H2, T1{});
           step(k + 1, s0 + k + 1, false, H2, H, T1{});
+        }
+      } else if (!track_block) {
+#pragma unroll 1
+        for (int k = 0; k < 32; k += 2) {
+          step(k, s0 + k, true, H, H2, T0{});
+          step(k + 1, s0 + k + 1, true, H2, H, T0{});
         }
       } else {
 #pragma unroll 1
