@@ -251,7 +251,9 @@ int32_t swb_measure_int_peak(swb_ctx* ctx, swb_int_peak* out);
  * (0 = automatic, else an instantiated rows-per-lane), "x2" (1 = allow the
  * packed 16x2 score-pass kernel), "x2_R" (its rows per lane, 0 = automatic),
  * "mm_prune" (corner-target pruning in Myers-Miller halves), "claim_mode"
- * (0 auto, 1 CTA claiming, 2 warp claiming), "proto", "reset_debug". */
+ * (0 auto, 1 CTA claiming, 2 warp claiming), "proto", "reset_debug",
+ * "job_major", "bound_maps", "live_ranges", "p2_R", "mm_R", "mm_static",
+ * "mm_dyn", "chain_wait" (acquire polling in chain-shaped passes). */
 int32_t swb_set_option(swb_ctx* ctx, const char* name, int64_t value);
 /* Current value of a tuning option (-1 for an unknown name). */
 int64_t swb_get_option(swb_ctx* ctx, const char* name);

@@ -107,6 +107,7 @@ struct PassParams {
   uint32_t tlo[8], thi[8];  // profile word per column code
   const int2* item_map;     // claim order -> (job, strip); null: job-major by item_base
   int32_t warp_claim;       // 1: per-warp claiming even for few jobs (range-limited passes)
+  int32_t chain_wait;       // chain-shaped passes: poll with ld.acquire, short back-off
   int32_t big;              // substitution table mode (tab) instead of tlo/thi
   const int32_t* tab;       // 32 x 33 table, device (big schemes)
 };
@@ -190,6 +191,22 @@ __device__ __forceinline__ int ld_relaxed(const int32_t* p) {
 #define SWB_WAIT_CAP_NS 256
 #endif
 constexpr unsigned kWaitCapNs = SWB_WAIT_CAP_NS;
+constexpr unsigned kFarWaitCapNs = 2048;  // producer not started: it is strips away
+
+// Chain-shaped passes (phase 2, Myers-Miller halves: a few strips in flight,
+// each waiting on its producer at every block): poll with ld.acquire so the
+// successful poll is the acquire (one L2 round trip instead of two), and keep
+// the back-off short (the poller is alone on its sub-partition).
+__device__ __forceinline__ int wait_acquire(const int32_t* p, int need) {
+  int v = ld_acquire(p);
+  unsigned ns = 0;
+  while (v < need) {
+    if (ns) __nanosleep(ns);
+    ns = ns ? (ns < 64 ? ns * 2 : 64) : 16;
+    v = ld_acquire(p);
+  }
+  return v;
+}
 __device__ __forceinline__ void wait_progress(const int32_t* p, int need, bool sys = false) {
   unsigned ns = 32;
   while ((sys ? ld_relaxed_sys(p) : ld_relaxed(p)) < need) {
@@ -501,22 +518,30 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     // The producer stores its live lo before the progress release that covers
     // it and its live hi before its final release, so "no live output" is only
     // concluded after acquiring the final progress.
+    // Most warps of a chain-shaped pass sit here, strips ahead of the front:
+    // they poll relaxed (an acquire per poll invalidates L1 and, summed over
+    // a thousand warps, loads L2 under the strips that do compute) and back
+    // off further while their producer has not even started.
     unsigned ns = 32;
     for (;;) {
-      const int p = ld_acquire(up_progress);
-      const int ax = ld_relaxed(&J.alive[s - 1].x);
-      if (ax > 0) {
-        alo_p = ax - 1;
-        break;
-      }
-      if (p >= cep) {
-        const int ay = ld_relaxed(&J.alive[s - 1].y);
-        alo_p = 0x7fffffff;
-        if (ay > 0) ahi_p = ay - 1;
-        break;
+      const int p0 = ld_relaxed(up_progress);
+      if (p0 >= cep || ld_relaxed(&J.alive[s - 1].x) > 0) {
+        const int p = ld_acquire(up_progress);
+        const int ax = ld_relaxed(&J.alive[s - 1].x);
+        if (ax > 0) {
+          alo_p = ax - 1;
+          break;
+        }
+        if (p >= cep) {
+          const int ay = ld_relaxed(&J.alive[s - 1].y);
+          alo_p = 0x7fffffff;
+          if (ay > 0) ahi_p = ay - 1;
+          break;
+        }
       }
       __nanosleep(ns);
-      ns = ns < kWaitCapNs ? ns * 2 : kWaitCapNs;
+      const unsigned cap = (P.chain_wait && p0 == 0) ? kFarWaitCapNs : kWaitCapNs;
+      ns = ns < cap ? ns * 2 : cap;
     }
     if (alo_p >= ahi_p || alo_p >= ce) cb = ce;
     else if (alo_p > cb) cb = alo_p;
@@ -705,7 +730,17 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       }
       if (!first && s0 < cep && s0 + 32 > cbp) {
         const int need = (s0 + 32 < cep) ? s0 + 32 : cep;
-        if (known_prog < need) {
+        if (known_prog < need && P.chain_wait && !ext_in) {
+          unsigned long long a0, a1;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a0));
+          known_prog = wait_acquire(up_progress, need);
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a1));
+          gw += a1 - a0;
+          if (dyn && ahi_p == 0x7fffffff) {
+            const int ay = ld_relaxed(&J.alive[s - 1].y);
+            if (ay > 0) ahi_p = ay - 1;
+          }
+        } else if (known_prog < need) {
           if ((ext_in ? ld_relaxed_sys(up_progress) : ld_relaxed(up_progress)) < need) {
             const long long tw = clock64();
             unsigned long long a0, a1;
@@ -886,8 +921,12 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       if (s >= 2 && !ext_out) {
         const int hi = s0 + 1 < ce ? s0 + 1 : ce;
         if (hi > cb && known_prog2 < hi) {
-          if (ld_relaxed(J.progress + (s - 2)) < hi) wait_progress(J.progress + (s - 2), hi);
-          known_prog2 = ld_acquire(J.progress + (s - 2));
+          if (P.chain_wait) {
+            known_prog2 = wait_acquire(J.progress + (s - 2), hi);
+          } else {
+            if (ld_relaxed(J.progress + (s - 2)) < hi) wait_progress(J.progress + (s - 2), hi);
+            known_prog2 = ld_acquire(J.progress + (s - 2));
+          }
         }
       }
       if (c >= cb && c < ce) __stcg(outbuf + c, sm->out[lane]);

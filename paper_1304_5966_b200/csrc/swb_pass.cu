@@ -570,6 +570,7 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     // spread their strips over warps and interleave the jobs (no pairing)
     for (size_t t = g0; t < g1; ++t)
       if (reqs[order[t]].rmap_fwd) P.warp_claim = 1;
+    P.chain_wait = P.warp_claim && ctx->chain_wait;
     memcpy(P.tlo, sc.tlo, sizeof(P.tlo));
     memcpy(P.thi, sc.thi, sizeof(P.thi));
 
@@ -752,6 +753,7 @@ extern "C" int64_t swb_get_option(swb_ctx* ctx, const char* name) {
   if (!strcmp(name, "mm_R")) return ctx->mm_R;
   if (!strcmp(name, "mm_static")) return ctx->mm_static;
   if (!strcmp(name, "mm_dyn")) return ctx->mm_dyn;
+  if (!strcmp(name, "chain_wait")) return ctx->chain_wait;
   if (!strcmp(name, "live_ranges")) return ctx->live_ranges;
   if (!strcmp(name, "p2_R")) return ctx->p2_R;
   if (!strcmp(name, "mm_prune")) return ctx->mm_prune;
@@ -785,6 +787,10 @@ extern "C" int32_t swb_set_option(swb_ctx* ctx, const char* name, int64_t value)
   }
   if (!strcmp(name, "mm_dyn")) {
     ctx->mm_dyn = (int)value;
+    return SWB_OK;
+  }
+  if (!strcmp(name, "chain_wait")) {
+    ctx->chain_wait = (int)value;
     return SWB_OK;
   }
   if (!strcmp(name, "mm_static")) {
