@@ -170,6 +170,11 @@ int32_t swb_seq_upload(swb_ctx* ctx, const uint8_t* codes, int64_t n, int32_t* s
   }
   swb_seq& sq = ctx->seqs[slot];
   sq.n = n;
+  {
+    uint8_t c4 = 0;
+    for (int64_t x = 0; x < n; ++x) c4 |= (uint8_t)(codes[x] == 4);
+    sq.has_code4 = c4 != 0;
+  }
   if (n > 0) {
     SWB_CUDA(cudaMemcpyAsync(sq.fwd, codes, (size_t)n, cudaMemcpyHostToDevice, ctx->stream));
     int blocks = (int)((n + 255) / 256);

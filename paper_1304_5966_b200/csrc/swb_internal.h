@@ -22,6 +22,7 @@ struct swb_seq {
   int64_t n = 0;
   int64_t cap = 0;  // allocated bytes of fwd / rev
   bool live = false;
+  bool has_code4 = false;  // holds code 4 (the DNA wildcard 'N' of the default alphabet)
 };
 
 // A grow-only device scratch buffer.

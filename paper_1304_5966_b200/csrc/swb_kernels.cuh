@@ -108,6 +108,7 @@ struct PassParams {
   const int2* item_map;     // claim order -> (job, strip); null: job-major by item_base
   int32_t warp_claim;       // 1: per-warp claiming even for few jobs (range-limited passes)
   int32_t chain_wait;       // chain-shaped passes: poll with ld.acquire, short back-off
+  int32_t wild_const;       // packed kernel, WILD: sub + go + ge of code-4 rows (any column)
   int32_t big;              // substitution table mode (tab) instead of tlo/thi
   const int32_t* tab;       // 32 x 33 table, device (big schemes)
 };

@@ -193,20 +193,22 @@ constexpr int kX2SlabR = 16;  // multigpu.SLAB_ROWS_PER_LANE x 32 rows = 64 x 16
 
 template <int R>
 int dispatch_x2_R(swb_ctx* ctx, const PassParams* P, long long items, int ctas_per_sm,
-                  int* occ_out) {
+                  int* occ_out, bool wild) {
   if (occ_out)
-    return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ_out, pass_kernel_x2<R>, 128, 0);
-  return launch_any(ctx, pass_kernel_x2<R>, *P, items, ctas_per_sm);
+    return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ_out, pass_kernel_x2<R, false>,
+                                                              128, 0);
+  return wild ? launch_any(ctx, pass_kernel_x2<R, true>, *P, items, ctas_per_sm)
+              : launch_any(ctx, pass_kernel_x2<R, false>, *P, items, ctas_per_sm);
 }
 
 int dispatch_x2(swb_ctx* ctx, int R, const PassParams* P, long long items, int ctas_per_sm,
-                int* occ_out) {
+                int* occ_out, bool wild = false) {
   switch (R) {
-    case 8: return dispatch_x2_R<8>(ctx, P, items, ctas_per_sm, occ_out);
-    case 10: return dispatch_x2_R<10>(ctx, P, items, ctas_per_sm, occ_out);
-    case 12: return dispatch_x2_R<12>(ctx, P, items, ctas_per_sm, occ_out);
-    case 14: return dispatch_x2_R<14>(ctx, P, items, ctas_per_sm, occ_out);
-    case 16: return dispatch_x2_R<16>(ctx, P, items, ctas_per_sm, occ_out);
+    case 8: return dispatch_x2_R<8>(ctx, P, items, ctas_per_sm, occ_out, wild);
+    case 10: return dispatch_x2_R<10>(ctx, P, items, ctas_per_sm, occ_out, wild);
+    case 12: return dispatch_x2_R<12>(ctx, P, items, ctas_per_sm, occ_out, wild);
+    case 14: return dispatch_x2_R<14>(ctx, P, items, ctas_per_sm, occ_out, wild);
+    case 16: return dispatch_x2_R<16>(ctx, P, items, ctas_per_sm, occ_out, wild);
     default: break;
   }
   return swb_fail(SWB_EINVAL, "packed rows_per_lane %d not instantiated", R);
@@ -352,10 +354,20 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
   // warp's window (<= 1024 rows + 96 columns, plus 32 columns of growth) lies
   // within kX2Span of the window maximum and the relative frame never clamps one.
   const long long ms = std::max(sc.max_sub, 0);
-  bool x2_scheme = sc.k <= 4 && !sc.big && ctx->x2_enabled && 95 * ms <= 1021 &&
-                   1120LL * (sc.goe + ms) + 32LL * ms + sc.goe <= 25000;
+  // Five codes are allowed when code 4 scores the same against every column
+  // (the default DNA alphabet's 'N' wildcard): its rows take a constant added
+  // in the cell update instead of a profile byte (swb_x2.cuh, WILD).
+  int wild_const = -1;
+  if (sc.k == 5 && !sc.big) {
+    wild_const = (int)(sc.thi[0] & 0xff);
+    for (int b = 0; b < 5; ++b)
+      if ((int)(sc.thi[b] & 0xff) != wild_const) wild_const = -1;
+    if (wild_const > 127) wild_const = -1;
+  }
+  bool x2_scheme = (sc.k <= 4 || wild_const >= 0) && !sc.big && ctx->x2_enabled &&
+                   95 * ms <= 1021 && 1120LL * (sc.goe + ms) + 32LL * ms + sc.goe <= 25000;
   for (int b = 0; b < sc.k && x2_scheme; ++b)
-    for (int a = 0; a < sc.k; ++a) {
+    for (int a = 0; a < 4 && a < sc.k; ++a) {
       const int v = (int)(int8_t)((sc.tlo[b] >> (8 * a)) & 0xff);
       if (v < 0 || v > 127) x2_scheme = false;
     }
@@ -366,9 +378,10 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
            // it only fixes the strip granularity (64 x kX2SlabR rows here)
            (r.force_R == 0 || r.ext_in || r.ext_out) &&
            (!r.ext_out || r.n1 % (64 * kX2SlabR) == 0);  // slab bottom row = item bottom row
+  for (PassReq& r : reqs) r.x2_wild = r.x2 && sc.k == 5 && r.rows_code4;
   // one launch per (recurrence, tracking, kernel) class; rows-per-lane per class
   auto cls = [&](int q) {
-    return (reqs[q].x2 ? 100 : 0) + (reqs[q].local ? 10 : 0) + reqs[q].track;
+    return (reqs[q].x2_wild ? 200 : reqs[q].x2 ? 100 : 0) + (reqs[q].local ? 10 : 0) + reqs[q].track;
   };
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cls(a) < cls(b); });
   std::vector<int> cls_ctas(reqs.size(), 0);
@@ -577,7 +590,8 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     SWB_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
     int rc;
     int ctas = ctx->max_ctas_per_sm ? ctx->max_ctas_per_sm : cls_ctas[order[g0]];
-    rc = head.x2  ? dispatch_x2(ctx, R, &P, item, ctas, nullptr)
+    P.wild_const = wild_const;
+    rc = head.x2  ? dispatch_x2(ctx, R, &P, item, ctas, nullptr, head.x2_wild)
          : sc.big ? dispatch_big(ctx, R, &P, item, head.local, head.track, ctas, nullptr)
                   : dispatch(ctx, R, &P, item, head.local, head.track, ctas, nullptr);
     if (rc) return rc;
@@ -846,6 +860,7 @@ extern "C" int32_t swb_pass(swb_ctx* ctx, const swb_scheme* scheme, const swb_pa
     const swb_pass_desc& d = descs[q];
     PassReq& r = reqs[q];
     rc = swb_resolve_seq(ctx, d.seq1, d.off1, d.len1, d.rev1, &r.rows, &r.rstep);
+    if (rc == SWB_OK) r.rows_code4 = ctx->seqs[d.seq1].has_code4;
     if (rc) return rc;
     rc = swb_resolve_seq(ctx, d.seq2, d.off2, d.len2, d.rev2, &r.cols, &r.cstep);
     if (rc) return rc;

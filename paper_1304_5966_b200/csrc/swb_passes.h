@@ -51,6 +51,8 @@ struct PassReq {
   // filled by swb_run_passes
   int R = 0;
   bool x2 = false;  // packed 16x2 phase-1 kernel
+  bool rows_code4 = false;  // the row sequence holds code 4
+  bool x2_wild = false;     // packed kernel with the constant-row wildcard (code 4)
   int nstrips = 0;
   long long res_offset = 0;
   long long best_score = 0, best_i = -1, best_j = -1;

@@ -45,8 +45,10 @@
 // fills A's half; the other lanes compute IMAD(shfl(x), 1, 0).
 //
 // Scope: local passes, TRACK_MIN, no band, no final rows, alphabets of <= 4
-// codes with 0 <= sub + go + ge <= 127, whole passes or row slabs whose
-// rows are a multiple of 64R.  Everything else uses run_strip.
+// codes with 0 <= sub + go + ge <= 127 (plus a fifth code that scores the same
+// against every column: the default DNA alphabet's 'N', WILD instantiation),
+// whole passes or row slabs whose rows are a multiple of 64R.  Everything else
+// uses run_strip.
 #pragma once
 
 #include "swb_kernels.cuh"
@@ -82,7 +84,7 @@ __device__ __forceinline__ int clamp_rel(long long v) {
   return v < 0 ? 0 : (v > 32767 ? 32767 : (int)v);
 }
 
-template <int R>
+template <int R, bool WILD>
 __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& Jg, int s,
                                           WarpSmemX2* sm, const uint32_t* __restrict__ tw_s) {
   static_assert(R <= 32, "rank field is 5 bits");
@@ -113,12 +115,20 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
 
   // selectors: byte0 <- T[colA] byte a, byte2 <- T[colB] byte b, bytes 1 and 3
   // replicate the (zero) sign of a profile byte; padding rows select zeros.
+  // WILD: code-4 rows select zeros like padding rows and take the scheme's
+  // constant through wadj (added with the diagonal), so a profile word still
+  // holds 4 codes.
   uint32_t sel[R];
+  uint32_t wadj[WILD ? R : 1];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int ia = rowA + r, ib = rowB + r;
-    const uint32_t a = (ia < n1) ? (uint32_t)J.rows[(long long)ia * J.rstep] : 8u;
-    const uint32_t b = (ib < n1) ? 4u + (uint32_t)J.rows[(long long)ib * J.rstep] : 8u;
+    uint32_t a = (ia < n1) ? (uint32_t)J.rows[(long long)ia * J.rstep] : 8u;
+    uint32_t b = (ib < n1) ? 4u + (uint32_t)J.rows[(long long)ib * J.rstep] : 8u;
+    if (WILD) {
+      wadj[r] = (a == 4u ? (uint32_t)P.wild_const : 0u) | (b == 8u && ib < n1 ? (uint32_t)P.wild_const << 16 : 0u);
+      if (a == 4u) a = 8u;
+    }
     sel[r] = a | ((a | 8u) << 4) | (b << 8) | ((b | 8u) << 12);
   }
   // Every profile word an inactive half may read must be a valid one: a byte
@@ -217,7 +227,7 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const uint32_t sv = prmt(tl, th, sel[r]);
-      const uint32_t ds = (uint32_t)imad((int)d, 1, (int)sv);
+      const uint32_t ds = WILD ? d + sv + wadj[r] : (uint32_t)imad((int)d, 1, (int)sv);
       const uint32_t h2 = vimax3_2(ds, E[r], FLOOR2);
       fv = viaddmax_2(fv, NGE2, hab);
       const uint32_t h2m = (uint32_t)imad((int)h2, 1, NGOE32);
@@ -551,7 +561,7 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
   }
 }
 
-template <int R>
+template <int R, bool WILD>
 __global__ void __launch_bounds__(256, 1) pass_kernel_x2(const PassParams P) {
   __shared__ WarpSmemX2 wsm[8];
   __shared__ uint32_t tw_s[8];
@@ -564,7 +574,7 @@ __global__ void __launch_bounds__(256, 1) pass_kernel_x2(const PassParams P) {
   auto run = [&](long long item) {
     int s = 0;
     const int j = item_job(P, item, &s);
-    run_strip_x2<R>(P, P.jobs[j], s, sm, tw_s);
+    run_strip_x2<R, WILD>(P, P.jobs[j], s, sm, tw_s);
   };
   if (P.group > 0) {
     const int w = (int)(blockDim.x >> 7);

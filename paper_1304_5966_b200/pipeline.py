@@ -49,7 +49,8 @@ def _report_phase1(report, scored, p1, S):
         report.update(score=scored.score, total_blocks=p1.total_blocks,
                       pruned_blocks=p1.pruned_blocks,
                       pruned_fraction=p1.pruned_blocks / max(1, p1.total_blocks),
-                      cells_executed=p1.cells_executed, kernel_ms=p1.kernel_ms)
+                      cells_executed=p1.cells_executed, kernel_ms=p1.kernel_ms, kernel=p1.kernel,
+                      rows_per_lane=p1.rows_per_lane)
 
 
 def align(seq1: Sequence, seq2: Sequence, scheme: ScoringScheme,

@@ -101,3 +101,35 @@ def test_x2_invariant_to_shape(n, seed):
         for k, v in saved.items():
             ctx.set_option(k, v)
     assert len(res) == 1, res
+
+
+@pytest.mark.parametrize("seed,n1,n2,frac", [(21, 3000, 2900, 0.02), (22, 60_000, 58_000, 0.001),
+                                             (23, 1100, 40_000, 0.3)])
+def test_x2_wildcard_rows(seed, n1, n2, frac):
+    """The default DNA alphabet ('N' = code 4 scores 0 against everything):
+    rows holding N run the packed kernel's WILD variant; same (score, end) as
+    the 32-bit kernel and the oracle, and the full alignment matches too."""
+    from paper_1304_5966_b200 import Alphabet
+    rng = np.random.default_rng(seed)
+    alpha = Alphabet.dna()
+    scheme = swb.ScoringScheme.match_mismatch(alpha, 1, -3, 5, 2)
+    a = random_codes(rng, n1)
+    b = mutate_codes(rng, a, 0.1)[:n2]
+    if b.size < n2:
+        b = np.concatenate([b, random_codes(rng, n2 - b.size)])
+    for arr in (a, b):
+        arr[rng.random(arr.size) < frac] = 4
+        st = int(rng.integers(0, arr.size - 50))
+        arr[st:st + 50] = 4
+    got = _both(a, b, scheme)
+    assert got[0] == got[1]
+    rep = {}
+    swb.score_only(Sequence.from_codes("a", a, alpha), Sequence.from_codes("b", b, alpha), scheme,
+                   report=rep)
+    assert rep["kernel"] == "packed16x2"
+    if n1 * n2 <= 2e8:
+        want = oracle.align(a, b, oracle_scheme(scheme))
+        summ, path = swb.align(Sequence.from_codes("a", a, alpha), Sequence.from_codes("b", b, alpha),
+                               scheme)
+        assert (summ.score, tuple(summ.start), tuple(summ.end)) == want[:3]
+        assert np.array_equal(path.ops, want[3])
