@@ -191,11 +191,14 @@ def align_e2e(swb, scheme, cpu_gcups, with_cpu: bool):
     a, b = synthetic_pair(5_000_000, seed=1003)
     s1 = swb.Sequence.from_codes("target", a, scheme.alphabet)
     s2 = swb.Sequence.from_codes("query", b, scheme.alphabet)
+    t0 = time.perf_counter()
+    swb.align(s1, s2, scheme)
+    first = time.perf_counter() - t0  # includes lazy loading of the phase-2/3 kernels
     rep = {}
     t0 = time.perf_counter()
     summ, path = swb.align(s1, s2, scheme, report=rep)
     dt = time.perf_counter() - t0
-    c3 = {"pair": "5 Mbp x 5 Mbp, mutate 10%, seed 1003", "gpu_s": dt,
+    c3 = {"pair": "5 Mbp x 5 Mbp, mutate 10%, seed 1003", "gpu_s": dt, "gpu_s_first_call": first,
           "phase_s": [round(x, 3) for x in rep.get("phase_seconds", [])], "score": summ.score,
           "start": list(summ.start), "end": list(summ.end), "path_ops": int(path.ops.size)}
     if cpu_gcups:
@@ -246,7 +249,7 @@ def run_multi(args, rank, world, local, dist):
                                               ipc_import, merge_best, slab_partition, slab_spec)
     a, b = synthetic_pair(args.n * world, seed=1002, homologous=not args.unrelated)
     b = b[:args.n]
-    scheme = swb.ScoringScheme.match_mismatch(swb.Alphabet.dna(wildcard=False), 1, -3, 5, 2)
+    scheme = swb.ScoringScheme.match_mismatch(swb.Alphabet.dna(), 1, -3, 5, 2)
     ctx = get_context(local)
     peak = ctx.measure_int_peak()
     ctx.set_option("rows_per_lane", SLAB_ROWS_PER_LANE)
@@ -373,7 +376,7 @@ def main():
     from paper_1304_5966_b200.engine import TRACK_MIN, Session, get_context
 
     a, b = synthetic_pair(args.n, seed=1002 + rank, homologous=not args.unrelated)
-    scheme = swb.ScoringScheme.match_mismatch(swb.Alphabet.dna(wildcard=False), 1, -3, 5, 2)
+    scheme = swb.ScoringScheme.match_mismatch(swb.Alphabet.dna(), 1, -3, 5, 2)
     ctx = get_context(0 if world == 1 else local)
     peak = ctx.measure_int_peak()
     cells = a.size * b.size
@@ -468,7 +471,8 @@ def main():
                                    "score + endpoint forward pass" if args.n == N_DEFAULT and
                                    not args.unrelated else
                                    f"{a.size} x {b.size} {'unrelated' if args.unrelated else 'homologous'} pair, score pass",
-                       "n1": int(a.size), "n2": int(b.size), "scheme": "match +1 / mismatch -3 / gap 5+2k",
+                       "n1": int(a.size), "n2": int(b.size),
+                       "scheme": "match +1 / mismatch -3 / gap 5+2k, default ACGT+N alphabet",
                        "prune": True, "l2": "flushed (512 MiB write) between timed steps",
                        "parallelism": "1 GPU" if world == 1 else f"{world} replicas (one pair per GPU)",
                        "score": res.best_score, "end": [res.best_i + 1, res.best_j + 1]},
