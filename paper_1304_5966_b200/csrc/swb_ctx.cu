@@ -23,13 +23,20 @@ int swb_fail(int code, const char* fmt, ...) {
   return code;
 }
 
+// Scratch grows geometrically: a Myers-Miller level doubles its subproblem
+// count, so a 25 % headroom would reallocate (cudaFree synchronises, pinned
+// host allocation is slow) at every level of the first alignment.
+static size_t grow_size(size_t bytes) {
+  return bytes < ((size_t)256 << 20) ? 4 * bytes : bytes + bytes / 4;
+}
+
 void* swb_scratch(swb_buf& b, size_t bytes) {
   if (bytes == 0) bytes = 256;
   if (b.cap >= bytes) return b.p;
   if (b.p) cudaFree(b.p);
   b.p = nullptr;
   b.cap = 0;
-  size_t want = bytes + bytes / 4;
+  size_t want = grow_size(bytes);
   if (cudaMalloc(&b.p, want) != cudaSuccess) {
     b.p = nullptr;
     cudaGetLastError();
@@ -45,7 +52,7 @@ void* swb_scratch_host(swb_buf& b, size_t bytes) {
   if (b.p) cudaFreeHost(b.p);
   b.p = nullptr;
   b.cap = 0;
-  size_t want = bytes + bytes / 4;
+  size_t want = grow_size(bytes);
   if (cudaMallocHost(&b.p, want) != cudaSuccess) {
     b.p = nullptr;
     cudaGetLastError();
