@@ -60,7 +60,8 @@ struct swb_ctx {
   int mm_R = 8;         // rows per lane of range-limited Myers-Miller passes
   int mm_static = 1;    // static strip ranges for Myers-Miller halves
   int mm_dyn = 1;       // per-block tile-bound skipping in Myers-Miller halves
-  int chain_wait = 1;   // acquire polling with short back-off in chain-shaped passes
+  int chain_wait = 1;
+  int chain_cta = 1;    // chain-shaped passes in chunks of 4 strips per CTA (shared-memory handoff)   // acquire polling with short back-off in chain-shaped passes
   swb_buf bmap_fwd, bmap_rev, bmap_live;
   // scratch
   swb_buf jobs, rowbuf, progress, results, finals, misc, host_pinned, flush;

@@ -109,6 +109,7 @@ struct PassParams {
   int32_t warp_claim;       // 1: per-warp claiming even for few jobs (range-limited passes)
   int32_t chain_wait;       // chain-shaped passes: poll with ld.acquire, short back-off
   int32_t wild_const;       // packed kernel, WILD: sub + go + ge of code-4 rows (any column)
+  int32_t chunk;            // > 0: CTA claims `chunk` consecutive strips (item_map: job, first)
   int32_t big;              // substitution table mode (tab) instead of tlo/thi
   const int32_t* tab;       // 32 x 33 table, device (big schemes)
 };
@@ -451,6 +452,18 @@ struct WarpSmem {
   int2 out[32];   // lane-31 outputs of the current 32-step block
 };
 
+// Chain chunks: a CTA runs 4 consecutive strips of one
+// chain, and each producer strip also hands its bottom row to the consumer
+// warp of the same CTA through shared memory: a 128-column ring plus the
+// published column, read as a seqlock (a column older than prog - 96 may be
+// overwritten by the block in flight and is read from the global row buffer,
+// which keeps the full protocol of §3.2).  prog = INT_MAX: producer done.
+struct ChainChan {
+  int2 buf[128];
+  volatile int prog;
+  volatile int ahi;  // mirror of alive[s].y (0 = unknown)
+};
+
 // Best-cell tracking without a slow path: every cell's H is folded with its
 // row into a 32-bit key (H - go - ge) * 32 + rank, rank = 31 - r (TRACK_MIN,
 // smaller row wins ties) or r (TRACK_MAX, larger row wins), so one max over
@@ -465,7 +478,8 @@ constexpr int kKeyClamp = -(1 << 25);
 template <int R, bool LOCAL, int TRACK, bool FINAL, bool BIG>
 __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, int s,
                                        WarpSmem* sm, const uint32_t* __restrict__ tlo_s,
-                                       const uint32_t* __restrict__ thi_s) {
+                                       const uint32_t* __restrict__ thi_s,
+                                       ChainChan* cin = nullptr, ChainChan* cout = nullptr) {
   const int* __restrict__ tab_s = reinterpret_cast<const int*>(tlo_s);  // BIG: the table
   const JobDev J = Jg;
   const int lane = threadIdx.x & 31;
@@ -559,6 +573,11 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       if (ext_out) st_release_sys(my_progress, 0x7fffffff);
       else st_release(my_progress, 0x7fffffff);
       J.strip_res[s] = make_int4(0, -1, -1, 0);
+      if (cout) {
+        cout->ahi = cb + 1;
+        __threadfence_block();
+        cout->prog = 0x7fffffff;
+      }
     }
     return;
   }
@@ -714,7 +733,10 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     if (dyn && (J.live_mode & 2) && prev_skipped && ahi_p < s0) {
       exited = true;
       exit_col = s0;
-      if (lane == 0) J.alive[s].y = (s0 - 31 > cb ? s0 - 31 : cb) + 1;
+      if (lane == 0) {
+        J.alive[s].y = (s0 - 31 > cb ? s0 - 31 : cb) + 1;
+        if (cout) cout->ahi = (s0 - 31 > cb ? s0 - 31 : cb) + 1;
+      }
       break;
     }
     // (1) stage lane-0 inputs and profile words for columns [s0, s0 + 32).
@@ -731,7 +753,23 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       }
       if (!first && s0 < cep && s0 + 32 > cbp) {
         const int need = (s0 + 32 < cep) ? s0 + 32 : cep;
-        if (known_prog < need && P.chain_wait && !ext_in) {
+        if (known_prog < need && cin) {
+          unsigned long long a0, a1;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a0));
+          int v = cin->prog;
+          while (v < need) {
+            __nanosleep(20);
+            v = cin->prog;
+          }
+          __threadfence_block();
+          known_prog = v;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a1));
+          gw += a1 - a0;
+          if (dyn && ahi_p == 0x7fffffff) {
+            const int ay = cin->ahi;
+            if (ay > 0) ahi_p = ay - 1;
+          }
+        } else if (known_prog < need && P.chain_wait && !ext_in) {
           unsigned long long a0, a1;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a0));
           known_prog = wait_acquire(up_progress, need);
@@ -764,7 +802,14 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
           th = top_h(J.border, c + 1, go, ge) - goe;
           tf = SWB_NEG32;
         } else if (c >= cbp && c < cep && c >= alo_p && c < ahi_p) {
-          int2 v = __ldcg(inbuf + c);
+          int2 v;
+          if (cin) {
+            v = cin->buf[c & 127];
+            __threadfence_block();
+            if (c < cin->prog - 96) v = __ldcg(inbuf + c);  // slot may have been reused
+          } else {
+            v = __ldcg(inbuf + c);
+          }
           th = v.x;
           tf = v.y;
         } else {
@@ -952,6 +997,14 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
           else st_release(my_progress, pub);
         }
       }
+      if (cout) {
+        if (c >= cb && c < ce) cout->buf[c & 127] = sm->out[lane];
+        __syncwarp();
+        __threadfence_block();
+        int pub = s0 + 1;
+        if (pub > ce) pub = ce;
+        if (lane == 0 && pub >= cb) cout->prog = pub;
+      }
     }
 
     // (5) running best for pruning (monotone, never ahead of the truth).
@@ -974,6 +1027,11 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     if (dyn && !exited) J.alive[s].y = ce + 1;
     if (ext_out) st_release_sys(my_progress, 0x7fffffff);
     else st_release(my_progress, 0x7fffffff);
+    if (cout) {
+      if (dyn && !exited) cout->ahi = ce + 1;
+      __threadfence_block();
+      cout->prog = 0x7fffffff;
+    }
   }
 
   // Strip result: decode the key, then warp reduction with the mode's tie
@@ -1037,6 +1095,17 @@ __device__ __forceinline__ void run_item(const PassParams& P, long long item, Wa
     run_strip<R, LOCAL, TRACK, false, BIG>(P, J, s, sm, tlo_s, thi_s);
 }
 
+template <int R, bool LOCAL, int TRACK, bool BIG>
+__device__ __forceinline__ void run_chunk_strip(const PassParams& P, const JobDev& J, int s,
+                                                WarpSmem* sm, const uint32_t* tlo_s,
+                                                const uint32_t* thi_s, ChainChan* cin,
+                                                ChainChan* cout) {
+  if (J.want_final && s == J.nstrips - 1)
+    run_strip<R, LOCAL, TRACK, true, BIG>(P, J, s, sm, tlo_s, thi_s, cin, cout);
+  else
+    run_strip<R, LOCAL, TRACK, false, BIG>(P, J, s, sm, tlo_s, thi_s, cin, cout);
+}
+
 // Persistent launch.  Two claiming modes:
 //  * P.group == 0: every warp claims one strip at a time (many small passes,
 //    e.g. a Myers-Miller level).
@@ -1061,6 +1130,30 @@ __global__ void __launch_bounds__(256) pass_kernel(const PassParams P) {
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   WarpSmem* sm = &wsm[warp];
+  if (P.chunk > 0) {
+    // chain chunks: 128 threads, warp w runs strip first + w of the claimed chunk
+    __shared__ ChainChan chan[4];
+    for (;;) {
+      if (threadIdx.x == 0) base_s = (long long)atomicAdd(P.claim, 1ULL);
+      if (lane == 0) {
+        chan[warp].prog = 0;
+        chan[warp].ahi = 0;
+      }
+      __syncthreads();
+      const long long c = base_s;
+      if (c >= P.total_items) break;
+      const int2 m = P.item_map[c];
+      const JobDev& J = P.jobs[m.x];
+      const int s = m.y + warp;
+      if (s < J.nstrips) {
+        ChainChan* cin = (warp > 0) ? &chan[warp - 1] : nullptr;
+        ChainChan* cout = (warp < 3 && s + 1 < J.nstrips) ? &chan[warp] : nullptr;
+        run_chunk_strip<R, LOCAL, TRACK, BIG>(P, J, s, sm, tlo_s, thi_s, cin, cout);
+      }
+      __syncthreads();
+    }
+    return;
+  }
   if (P.group > 0) {
     const int w = (int)(blockDim.x >> 7);
     for (;;) {

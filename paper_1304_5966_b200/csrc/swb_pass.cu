@@ -120,6 +120,14 @@ int launch_any(swb_ctx* ctx, K kern, const PassParams& Pin, long long items, int
   SWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, 0));
   if (per_sm < 1) return swb_fail(SWB_ECUDA, "pass kernel does not fit on an SM");
   if (ctas_per_sm > 0 && per_sm > ctas_per_sm) per_sm = ctas_per_sm;
+  if (P.chunk > 0) {
+    const long long cap = (long long)per_sm * ctx->sms;
+    const int grid = (int)std::min(cap, std::max((long long)P.total_items, 1LL));
+    kern<<<grid, 128, 0, ctx->stream>>>(P);
+    ctx->launches++;
+    SWB_CUDA(cudaGetLastError());
+    return SWB_OK;
+  }
   if (ctx->claim_mode != 2 && (ctx->claim_mode == 1 || (P.njobs <= 4 && !P.warp_claim)) &&
       per_sm <= 2 && items > (long long)ctx->sms * 4) {
     // one CTA per SM, per_sm warps per sub-partition, adjacent strips paired
@@ -534,9 +542,29 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
       item += r.nstrips;
       strip_off += r.nstrips;
     }
+    // Chain-shaped passes (a corridor from the tile maps: phase 2, Myers-Miller
+    // halves) with long chains run in chunks of 4 consecutive strips per CTA
+    // (swb_kernels.cuh ChainChan); the claim map then lists (job, first strip)
+    bool chain_chunks = false;
+    if (ctx->chain_cta && !head.x2) {
+      bool chainy = false, ext = false;
+      for (size_t t = g0; t < g1; ++t) {
+        chainy |= reqs[order[t]].rmap_fwd != nullptr || reqs[order[t]].bmap_in != nullptr;
+        ext |= reqs[order[t]].ext_in != nullptr || reqs[order[t]].ext_out != nullptr;
+      }
+      chain_chunks = chainy && !ext && total_strips >= 8LL * nj;
+    }
+    long long chunk_items = 0;
     // strip-major claim order across jobs (item_job in swb_kernels.cuh)
     int2* d_map = nullptr;
-    if (nj > 1 && !ctx->job_major) {  // (group-mode launches drop it, see launch_any)
+    if (chain_chunks) {
+      d_map = A.take<int2>(total_strips);
+      int max_strips = 0;
+      for (int t = 0; t < nj; ++t) max_strips = std::max(max_strips, h_jobs[t].nstrips);
+      for (int st = 0; st < max_strips; st += 4)
+        for (int t = 0; t < nj; ++t)
+          if (st < h_jobs[t].nstrips) h_map[chunk_items++] = make_int2(t, st);
+    } else if (nj > 1 && !ctx->job_major) {  // (group-mode launches drop it, see launch_any)
       d_map = A.take<int2>(total_strips);
       long long q = 0;
       int max_strips = 0;
@@ -552,8 +580,9 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
       SWB_CUDA(cudaMemcpyAsync(d_tab, sc.tab, sizeof(int32_t) * 32 * kTabStride,
                                cudaMemcpyHostToDevice, ctx->stream));
     if (d_map)
-      SWB_CUDA(cudaMemcpyAsync(d_map, h_map, sizeof(int2) * total_strips, cudaMemcpyHostToDevice,
-                               ctx->stream));
+      SWB_CUDA(cudaMemcpyAsync(d_map, h_map,
+                               sizeof(int2) * (chain_chunks ? chunk_items : total_strips),
+                               cudaMemcpyHostToDevice, ctx->stream));
     SWB_CUDA(cudaMemsetAsync(A.base + zero_begin, 0, zero_end - zero_begin, ctx->stream));
     bool any_final = false;
     for (int t = 0; t < nj && !any_final; ++t) any_final = reqs[order[g0 + t]].want_final;
@@ -584,6 +613,10 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     for (size_t t = g0; t < g1; ++t)
       if (reqs[order[t]].rmap_fwd) P.warp_claim = 1;
     P.chain_wait = P.warp_claim && ctx->chain_wait;
+    if (chain_chunks) {
+      P.chunk = 4;
+      P.total_items = chunk_items;
+    }
     memcpy(P.tlo, sc.tlo, sizeof(P.tlo));
     memcpy(P.thi, sc.thi, sizeof(P.thi));
 
@@ -768,6 +801,7 @@ extern "C" int64_t swb_get_option(swb_ctx* ctx, const char* name) {
   if (!strcmp(name, "mm_static")) return ctx->mm_static;
   if (!strcmp(name, "mm_dyn")) return ctx->mm_dyn;
   if (!strcmp(name, "chain_wait")) return ctx->chain_wait;
+  if (!strcmp(name, "chain_cta")) return ctx->chain_cta;
   if (!strcmp(name, "live_ranges")) return ctx->live_ranges;
   if (!strcmp(name, "p2_R")) return ctx->p2_R;
   if (!strcmp(name, "mm_prune")) return ctx->mm_prune;
@@ -805,6 +839,10 @@ extern "C" int32_t swb_set_option(swb_ctx* ctx, const char* name, int64_t value)
   }
   if (!strcmp(name, "chain_wait")) {
     ctx->chain_wait = (int)value;
+    return SWB_OK;
+  }
+  if (!strcmp(name, "chain_cta")) {
+    ctx->chain_cta = (int)value;
     return SWB_OK;
   }
   if (!strcmp(name, "mm_static")) {

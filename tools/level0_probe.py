@@ -37,10 +37,11 @@ with Session(ctx, a, b, sc) as S:
     print(f"phase 2 {time.perf_counter() - t0:.3f} s", flush=True)
     timeline("phase2")
     root = phase3._as_array([phase3.Subproblem(start, e, scored.score)], True)
-    for R in [int(x) for x in sys.argv[2:]] or (0, 8, 16, 32):
+    for R, cc in [(int(x), 1) for x in sys.argv[2:]] or ((0, 1), (0, 0), (8, 1), (16, 1)):
         ctx.set_option("rows_per_lane", R)
+        ctx.set_option("chain_cta", cc)
         t0 = time.perf_counter()
         res, cells = ctx.crossings(S.cs, S.s1, S.s2, root, True)
-        print(f"level0 R={R}: {time.perf_counter() - t0:.3f} s cells {cells:.3e} kernel {ctx.last_kernel_ms:.1f} ms", flush=True)
-        timeline(f"level0 R={R}")
+        print(f"level0 R={R} chain_cta={cc}: {time.perf_counter() - t0:.3f} s cells {cells:.3e} kernel {ctx.last_kernel_ms:.1f} ms", flush=True)
+        timeline(f"level0 R={R} cc={cc}")
     ctx.set_option("rows_per_lane", 0)

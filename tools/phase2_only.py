@@ -20,3 +20,15 @@ with Session(ctx, a, b, sc) as S:
     t0 = time.perf_counter()
     start = phase2.locate_start(S, e, scored.score, band)
     print(f"phase 2 {time.perf_counter() - t0:.3f} s kernel {ctx.last_kernel_ms:.1f} ms start {start}", flush=True)
+    import numpy as np
+    for opt, mc in ((1, 0), (0, 0), (1, 0), (0, 1), (0, 2), (1, 1), (1, 2)):
+        ctx.set_option("chain_cta", opt)
+        ctx.set_option("max_ctas_per_sm", mc)
+        t0 = time.perf_counter()
+        phase2.locate_start(S, e, scored.score, band)
+        t = ctx.debug_times().astype(np.float64)
+        st, en, wt = t[:, 0], t[:, 1], t[:, 2]
+        act = (en - st) / 1e3
+        print(f"chain_cta={opt} max_ctas={mc}: {time.perf_counter() - t0:.3f} s kernel {ctx.last_kernel_ms:.1f} ms strips {len(t)} "
+              f"active mean {act.mean():.1f} us wait mean {wt.mean() / 1e3:.1f} us "
+              f"wait by warp slot {[round(float(wt[k::4].mean() / 1e3), 1) for k in range(4)]}", flush=True)
