@@ -725,6 +725,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
   };
 
   bool prev_skipped = false, exited = false;
+  int lazy_pub = 0;
   int exit_col = 0;
   int known_prog2 = 0;  // progress of strip s-2 (previous writer of our buffer)
   for (int s0 = cb; s0 < s_end; s0 += 32) {
@@ -806,7 +807,10 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
           if (cin) {
             v = cin->buf[c & 127];
             __threadfence_block();
-            if (c < cin->prog - 96) v = __ldcg(inbuf + c);  // slot may have been reused
+            if (c < cin->prog - 96) {  // slot may have been reused: global row buffer
+              if (ld_acquire(up_progress) <= c) wait_acquire(up_progress, c + 1);
+              v = __ldcg(inbuf + c);
+            }
           } else {
             v = __ldcg(inbuf + c);
           }
@@ -992,7 +996,10 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       if (lane == 0) {
         int pub = s0 + 1;
         if (pub > ce) pub = ce;
-        if (pub >= cb) {
+        // a producer whose consumer reads the shared-memory ring releases the
+        // global progress every 4th block only (its readers: the consumer's
+        // start and ring fallback, strip s+2's buffer check)
+        if (pub >= cb && (!cout || pub >= ce || (++lazy_pub & 3) == 0)) {
           if (ext_out) st_release_sys(my_progress, pub);
           else st_release(my_progress, pub);
         }
