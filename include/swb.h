@@ -210,6 +210,10 @@ int32_t swb_bounds_reset(swb_ctx* ctx, int32_t seq1, int32_t seq2);
  * nr x nc, raw encoding (value + 2^30, -1 = never written) into out[0..cap);
  * returns nr * nc (the size when out is NULL). */
 int64_t swb_bounds_read(swb_ctx* ctx, int32_t which, int32_t* out, int64_t cap);
+/* Device address and element count (nr * nc) of the forward (1) or reverse
+ * (2) map, for collectives that assemble one map from the row slabs of several
+ * GPUs (multigpu.align_distributed).  Row tile t occupies [t * nc, (t+1) * nc). */
+int32_t swb_bounds_device(swb_ctx* ctx, int32_t which, uint64_t* ptr, int64_t* n, int64_t* nc);
 
 /* --- Myers-Miller level --------------------------------------------------------
  * For each subproblem (rows >= 2 required): run the upper forward and the

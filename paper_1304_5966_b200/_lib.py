@@ -76,7 +76,7 @@ EXPORTS = (
     "swb_last_kernel_ms", "swb_launch_count", "swb_set_option", "swb_get_option", "swb_debug_stats",
     "swb_debug_times", "swb_timer_start", "swb_timer_stop", "swb_flush_l2",
     "swb_boundary_alloc", "swb_boundary_reset", "swb_boundary_free", "swb_ipc_export",
-    "swb_ipc_import", "swb_ipc_close", "swb_bounds_reset", "swb_bounds_read",
+    "swb_ipc_import", "swb_ipc_close", "swb_bounds_reset", "swb_bounds_read", "swb_bounds_device",
 )
 
 _lib = None
@@ -114,6 +114,8 @@ def load() -> ctypes.CDLL:
         lib.swb_bounds_reset.restype = c_i32
         lib.swb_bounds_read.argtypes = [c_p, c_i32, c_p, c_i64]
         lib.swb_bounds_read.restype = c_i64
+        lib.swb_bounds_device.argtypes = [c_p, c_i32, P(ctypes.c_uint64), P(c_i64), P(c_i64)]
+        lib.swb_bounds_device.restype = c_i32
         lib.swb_leaves.argtypes = [c_p, P(Scheme), c_i32, c_i32, P(Subproblem), c_i32, c_i32,
                                    c_p, c_p, c_p, c_p]
         lib.swb_leaves.restype = c_i32

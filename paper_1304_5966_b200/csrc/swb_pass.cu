@@ -790,6 +790,20 @@ extern "C" int64_t swb_bounds_read(swb_ctx* ctx, int32_t which, int32_t* out, in
   return n;
 }
 
+extern "C" int32_t swb_bounds_device(swb_ctx* ctx, int32_t which, uint64_t* ptr, int64_t* n,
+                                     int64_t* nc) {
+  SWB_API_BEGIN(ctx);
+  if (!ptr || !n || !nc || (which != 1 && which != 2))
+    return swb_fail(SWB_EINVAL, "swb_bounds_device: bad arguments");
+  const swb_buf& b = which == 2 ? ctx->bmap_rev : ctx->bmap_fwd;
+  if (!b.p || ctx->bmap_seq1 < 0) return swb_fail(SWB_EINVAL, "no tile maps (swb_bounds_reset first)");
+  SWB_CUDA(cudaStreamSynchronize(ctx->stream));
+  *ptr = (uint64_t)(uintptr_t)b.p;
+  *n = (int64_t)ctx->bmap_nr * ctx->bmap_nc;
+  *nc = ctx->bmap_nc;
+  SWB_API_END();
+}
+
 extern "C" int64_t swb_get_option(swb_ctx* ctx, const char* name) {
   if (!ctx || !name) return -1;
   if (!strcmp(name, "max_ctas_per_sm")) return ctx->max_ctas_per_sm;

@@ -135,6 +135,13 @@ class DeviceContext:
             self.lib.swb_bounds_read(self.ptr, which, out.ctypes.data, n)
         return out
 
+    def bounds_device(self, which: int) -> tuple[int, int, int]:
+        """(device address, nr * nc, nc) of the forward (1) / reverse (2) map."""
+        p, n, nc = ctypes.c_uint64(), ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(self.lib.swb_bounds_device(self.ptr, which, ctypes.byref(p), ctypes.byref(n),
+                                              ctypes.byref(nc)), "swb_bounds_device")
+        return int(p.value), int(n.value), int(nc.value)
+
     def get_option(self, name: str) -> int:
         return int(self.lib.swb_get_option(self.ptr, name.encode()))
 

@@ -155,3 +155,112 @@ def run_slabs_sequential(S, slabs: list[Slab], prune: bool = True):
         S.ctx.set_option("rows_per_lane", 0)
         for b in bounds:
             b.free()
+
+
+class _DeviceRows:
+    """__cuda_array_interface__ view of int32 device memory (a tile-map slice)
+    so that torch / NCCL can move it without a copy."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": "<i4",
+                                         "data": (int(ptr), False), "version": 3,
+                                         "strides": None}
+
+
+def map_row_tiles(slab: Slab, tile_rows: int = 1024) -> tuple[int, int]:
+    """Forward-map row tiles [lo, hi) a slab's pass writes (slabs are cut in
+    multiples of 1024 rows, so neighbouring slabs never share a tile row)."""
+    return slab.row0 // tile_rows, -(-slab.row1 // tile_rows)
+
+
+def align_distributed(seq1, seq2, scheme, config=None, report: dict | None = None):
+    """Full alignment on all GPUs of a torch.distributed job (one process per
+    GPU, NCCL): the phase-1 score pass runs as row slabs with the boundary rows
+    streamed over NVLink peer memory; the per-slab bests merge
+    with the reference's tie rule; each GPU's slab of the forward tile map
+    (§3.6) is gathered into rank 0 over NCCL, and rank 0 runs phases 2 and 3
+    (chains along the path, §7) with the whole map.  Every rank returns the
+    same (summary, path), identical to pipeline.align() on one GPU."""
+    import os
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from . import phase1
+    from .engine import Session, get_context
+    from .model import AlignmentPath, AlignmentSummary, Coord, validate_scheme
+    from .pipeline import AlignConfig, finish
+    import time
+
+    cfg = config or AlignConfig()
+    if cfg.split != 1:
+        raise ValueError("align_distributed runs split=1 (the slab pipeline replaces split=2)")
+    if len(seq1) < 1 or len(seq2) < 1:
+        raise ValueError("alignment inputs must be non-empty")
+    scheme = validate_scheme(scheme)
+    rank, world = dist.get_rank(), dist.get_world_size()
+    local = int(os.environ.get("LOCAL_RANK", cfg.device))
+    torch.cuda.set_device(local)
+    ctx = get_context(local)
+    t0 = time.perf_counter()
+    with Session(ctx, seq1.codes, seq2.codes, scheme) as S:
+        S.reset_bounds()
+        slabs = slab_partition(S.n1, world, SLAB_STRIP_ROWS)
+        me = slabs[rank]
+        inbound = Boundary(ctx, S.n2) if rank > 0 else None
+        handles = [None] * world
+        dist.all_gather_object(handles, inbound.export() if inbound else None)
+        ext_out = None
+        if rank + 1 < world:
+            hb, hp = handles[rank + 1]
+            ext_out = (ipc_import(ctx, hb), ipc_import(ctx, hp))
+        ext_in = (inbound.buf, inbound.progress) if inbound else None
+        try:
+            dist.barrier()
+            if world > 1:
+                ctx.set_option("rows_per_lane", SLAB_ROWS_PER_LANE)
+            try:
+                spec = slab_spec(me, S.n1, S.n2, ext_in, ext_out, cfg.prune)
+                spec["bound_write"] = 1 if S.bounds else 0
+                res = S.run([spec])[0]
+            finally:
+                ctx.set_option("rows_per_lane", 0)
+            bests = [None] * world
+            dist.all_gather_object(bests, (res.best_score, res.best_i, res.best_j))
+            score, bi, bj = merge_best([tuple(b) for b in bests], TRACK_MIN)
+            scored = (phase1.ScoredEndpoint(score, Coord(bi + 1, bj + 1)) if score > 0
+                      else phase1.ScoredEndpoint(0, Coord(0, 0)))
+            # assemble the forward tile map on rank 0 (row tiles are disjoint)
+            if S.bounds and world > 1:
+                ptr, n, nc = ctx.bounds_device(1)
+                full = torch.as_tensor(_DeviceRows(ptr, n), device=f"cuda:{local}")
+                for g in range(1, world):
+                    lo, hi = map_row_tiles(slabs[g])
+                    if hi <= lo:
+                        continue
+                    part = full[lo * nc:hi * nc]
+                    if rank == g:
+                        dist.send(part, dst=0)
+                    elif rank == 0:
+                        dist.recv(part, src=g)
+                torch.cuda.synchronize()
+            out = [None]
+            if rank == 0:
+                summary, path = finish(S, scored, cfg, report, t0)
+                out[0] = (summary.score, tuple(summary.start), tuple(summary.end),
+                          tuple(path.start), path.ops.tobytes())
+            dist.broadcast_object_list(out, src=0)
+        finally:
+            dist.barrier()
+            if ext_out:
+                ctx.lib.swb_ipc_close(ctx.ptr, ext_out[0])
+                ctx.lib.swb_ipc_close(ctx.ptr, ext_out[1])
+            dist.barrier()
+            if inbound:
+                inbound.free()
+    sc, st, en, pst, ops = out[0]
+    if sc == 0:
+        return AlignmentSummary.empty(), AlignmentPath.empty()
+    return (AlignmentSummary(sc, Coord(*st), Coord(*en)),
+            AlignmentPath(Coord(*pst), np.frombuffer(ops, dtype=np.uint8).copy()))

@@ -71,23 +71,30 @@ def align(seq1: Sequence, seq2: Sequence, scheme: ScoringScheme,
         t0 = time.perf_counter()
         S.reset_bounds()  # tile bound maps for phases 2 and 3
         scored, p1 = phase1.best_local(S, cfg.prune)
-        t1 = time.perf_counter()
         _report_phase1(report, scored, p1, S)
-        if scored.score == 0:
-            return AlignmentSummary.empty(), AlignmentPath.empty()
-        band = None
-        if cfg.band:
-            e = scored.end
-            band = phase2.compute_band(scored.score, min(e.i, e.j), max(e.i, e.j), scheme)
-        start = phase2.locate_start(S, scored.end, scored.score, band)
-        t2 = time.perf_counter()
-        summary = AlignmentSummary(scored.score, start, scored.end)
-        path = phase3.reconstruct(S, summary, cfg.leaf_limit, cfg.band, stats=report)
-        t3 = time.perf_counter()
-        if report is not None:
-            report.update(device_kernel_ms=S.kernel_ms, device_cells=S.cells,
-                          phase_seconds=(t1 - t0, t2 - t1, t3 - t2))
-        return summary, path
+        return finish(S, scored, cfg, report, t0)
+
+
+def finish(S: Session, scored: phase1.ScoredEndpoint, cfg: AlignConfig, report: dict | None,
+           t0: float) -> tuple[AlignmentSummary, AlignmentPath]:
+    """Phases 2 and 3 after a phase-1 endpoint (pipeline.py:75-100); shared by
+    align() and multigpu.align_distributed()."""
+    t1 = time.perf_counter()
+    if scored.score == 0:
+        return AlignmentSummary.empty(), AlignmentPath.empty()
+    band = None
+    if cfg.band:
+        e = scored.end
+        band = phase2.compute_band(scored.score, min(e.i, e.j), max(e.i, e.j), S.scheme)
+    start = phase2.locate_start(S, scored.end, scored.score, band)
+    t2 = time.perf_counter()
+    summary = AlignmentSummary(scored.score, start, scored.end)
+    path = phase3.reconstruct(S, summary, cfg.leaf_limit, cfg.band, stats=report)
+    t3 = time.perf_counter()
+    if report is not None:
+        report.update(device_kernel_ms=S.kernel_ms, device_cells=S.cells,
+                      phase_seconds=(t1 - t0, t2 - t1, t3 - t2))
+    return summary, path
 
 
 def score_only(seq1: Sequence, seq2: Sequence, scheme: ScoringScheme,
