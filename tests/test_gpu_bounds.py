@@ -11,7 +11,7 @@ from paper_1304_5966_b200.engine import get_context
 
 pytestmark = pytest.mark.gpu
 
-OPTS = ("bound_maps", "mm_static", "mm_dyn", "live_ranges")
+OPTS = ("bound_maps", "mm_static", "mm_dyn", "live_ranges", "chain_cta", "chain_wait")
 
 
 def _align(a, b, scheme, **opts):
@@ -49,3 +49,20 @@ def test_bounds_with_other_schemes():
         sc = dna_scheme(None, *args)
         assert _align(a, b, sc, bound_maps=1, live_ranges=3) == _align(a, b, sc, bound_maps=0,
                                                                        live_ranges=0)
+
+
+@pytest.mark.parametrize("seed,n,rate", [(10, 9_000, 0.1), (11, 33_000, 0.2), (12, 130_000, 0.1),
+                                         (13, 70_000, 0.02)])
+def test_chain_chunks_exact(seed, n, rate):
+    """Chain chunks (4 strips per CTA, shared-memory ring with
+    a global fallback, lazy global release) and acquire polling change only
+    the schedule: identical results with each switched off, on strip counts
+    that are not multiples of 4 and with levels of many short jobs."""
+    rng = np.random.default_rng(seed)
+    a = random_codes(rng, n)
+    b = mutate_codes(rng, a, rate)[: n - 777]
+    sc = dna_scheme()
+    ref = _align(a, b, sc, chain_cta=0, chain_wait=0)
+    assert _align(a, b, sc, chain_cta=1, chain_wait=1) == ref
+    assert _align(a, b, sc, chain_cta=1, chain_wait=0) == ref
+    assert _align(a, b, sc, chain_cta=1, live_ranges=0) == ref
