@@ -257,7 +257,8 @@ int32_t swb_measure_int_peak(swb_ctx* ctx, swb_int_peak* out);
  * "mm_prune" (corner-target pruning in Myers-Miller halves), "claim_mode"
  * (0 auto, 1 CTA claiming, 2 warp claiming), "proto", "reset_debug",
  * "job_major", "bound_maps", "live_ranges", "p2_R", "mm_R", "mm_static",
- * "mm_dyn", "chain_wait" (acquire polling in chain-shaped passes). */
+ * "mm_dyn", "chain_wait" (acquire polling in chain-shaped passes),
+ * "chain_cta" (chain-shaped passes in CTA chunks of 4 strips). */
 int32_t swb_set_option(swb_ctx* ctx, const char* name, int64_t value);
 /* Current value of a tuning option (-1 for an unknown name). */
 int64_t swb_get_option(swb_ctx* ctx, const char* name);
