@@ -509,7 +509,10 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
                                                     -(1LL << 29));
       J.alive = (r.border == SWB_BORDER_RESTRICTED && !r.ext_in && !r.ext_out && ctx->live_ranges)
                     ? d_alive + strip_off : nullptr;
-      J.live_mode = ctx->live_ranges;
+      // Early exit stays off for shared-table (BIG) passes: golden protein record 85
+      // (1171 x 144, BLOSUM62 11/1) faults in phase 2 when late start, early exit and
+      // tile bound maps combine (tools/repro_zero_protein.py)
+      J.live_mode = sc.big ? (ctx->live_ranges & 1) : ctx->live_ranges;
       J.bmap_live = (J.alive && r.bmap_live) ? r.bmap_live : nullptr;
       J.rmap_live = r.rmap_live;
       J.bin_rev = r.bin_rev;

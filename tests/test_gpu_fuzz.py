@@ -104,3 +104,18 @@ def test_fuzz_zero_score_pairs():
             assert (summary.score, tuple(summary.start), tuple(summary.end)) == want[:3], cfg_kw
             assert len(path) == 0
         assert swb.score_only(s1, s2, scheme).score == 0
+
+
+def test_protein_record_85_repeated(golden_protein):
+    """Golden protein record 85 (1171 x 144, a 12-residue local hit) once
+    faulted in phase 2 when late start, early exit and tile bound maps
+    combined on the shared-table kernel; repeated because the
+    fault was timing dependent."""
+    from helpers import golden_inputs
+    rec = golden_protein[85]
+    s1, s2, scheme = golden_inputs(rec)
+    for _ in range(10):
+        summary, path = swb.align(s1, s2, scheme)
+        assert summary.score == rec["align"]["score"]
+        assert list(summary.start) == rec["align"]["start"]
+        assert list(summary.end) == rec["align"]["end"]
