@@ -269,6 +269,18 @@ int32_t swb_debug_stats(swb_ctx* ctx, int64_t* out, int32_t n);
 /* Per-strip (start ns, end ns, wait ns) of the most recent pass launch; returns
  * the number of values available. */
 int32_t swb_debug_times(swb_ctx* ctx, int64_t* out, int32_t n);
+/* Per-strip record of the most recent pass launch, 12 values per strip:
+ * (cb_static << 32 | cb_start), (ce << 32 | early-exit column or -1),
+ * (blocks executed << 32 | blocks skipped), (live lo << 32 | live hi of the
+ * producer), times the strip was run, (smid << 32 | cta << 8 | warp), start
+ * ns, 0, then the strip result (score key, i, j, has).  Returns the number of
+ * values available (out may be null). */
+int32_t swb_debug_strips(swb_ctx* ctx, int64_t* out, int32_t n);
+/* Claim log (option "claim_log" or env SWB_CLAIM_LOG): out[0] = entries ever
+ * written, out[8 + 4k ...] = ring entry k (launch id, kind << 56 | smid << 40 |
+ * cta << 8 | warp, value, globaltimer ns); kind 1 = claimed item, 2 = claim
+ * counter at CTA start, 3 = progress of strip 0 at CTA start. */
+int32_t swb_debug_claims(swb_ctx* ctx, int64_t* out, int32_t n);
 
 /* CUDA events on the context's stream around a caller-defined region
  * (bench timing of K steps on the launching stream). */

@@ -74,7 +74,8 @@ EXPORTS = (
     "swb_ctx_create", "swb_ctx_destroy", "swb_last_error", "swb_version", "swb_seq_upload",
     "swb_seq_release", "swb_pass", "swb_crossings", "swb_leaves", "swb_measure_int_peak",
     "swb_last_kernel_ms", "swb_launch_count", "swb_set_option", "swb_get_option", "swb_debug_stats",
-    "swb_debug_times", "swb_timer_start", "swb_timer_stop", "swb_flush_l2",
+    "swb_debug_times", "swb_debug_strips", "swb_debug_claims",
+    "swb_timer_start", "swb_timer_stop", "swb_flush_l2",
     "swb_boundary_alloc", "swb_boundary_reset", "swb_boundary_free", "swb_ipc_export",
     "swb_ipc_import", "swb_ipc_close", "swb_bounds_reset", "swb_bounds_read", "swb_bounds_device",
 )
@@ -133,6 +134,10 @@ def load() -> ctypes.CDLL:
         lib.swb_debug_stats.restype = c_i32
         lib.swb_debug_times.argtypes = [c_p, c_p, c_i32]
         lib.swb_debug_times.restype = c_i32
+        lib.swb_debug_strips.argtypes = [c_p, c_p, c_i32]
+        lib.swb_debug_strips.restype = c_i32
+        lib.swb_debug_claims.argtypes = [c_p, c_p, c_i32]
+        lib.swb_debug_claims.restype = c_i32
         lib.swb_timer_start.argtypes = [c_p]
         lib.swb_timer_start.restype = c_i32
         lib.swb_timer_stop.argtypes = [c_p, ctypes.POINTER(ctypes.c_double)]

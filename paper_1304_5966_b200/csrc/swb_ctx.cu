@@ -100,6 +100,8 @@ swb_ctx* swb_ctx_create(int32_t device) {
   swb_ctx* ctx = new swb_ctx();
   ctx->device = device;
   ctx->trace = getenv("SWB_TRACE") != nullptr;
+  if (const char* w = getenv("SWB_WATCHDOG_MS")) ctx->watchdog_ms = atoi(w);
+  if (getenv("SWB_CLAIM_LOG")) ctx->claim_log_on = 1;
   ctx->sms = prop.multiProcessorCount;
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess) {
@@ -119,7 +121,8 @@ void swb_ctx_destroy(swb_ctx* ctx) {
     if (s.rev) cudaFree(s.rev);
   }
   swb_buf* bufs[] = {&ctx->jobs,  &ctx->rowbuf, &ctx->progress, &ctx->results, &ctx->finals,
-                     &ctx->misc,  &ctx->flush,  &ctx->bmap_fwd, &ctx->bmap_rev, &ctx->bmap_live};
+                     &ctx->misc,  &ctx->flush,  &ctx->bmap_fwd, &ctx->bmap_rev, &ctx->bmap_live,
+                     &ctx->pass_finals, &ctx->dbg_buf, &ctx->claim_log};
   if (ctx->tev0) {
     cudaEventDestroy(ctx->tev0);
     cudaEventDestroy(ctx->tev1);

@@ -38,6 +38,31 @@
 
 #include "swb_internal.h"
 
+// Debug build (make CHECKED=1 -> libswb_checked.so): every global and shared
+// index of the pass kernels goes through SWB_IX(i, n), which reports an index
+// outside [0, n) with its source line and substitutes 0, so the run continues
+// and every bad access of a launch is listed.  Compiled out otherwise.
+#ifdef SWB_CHECKED
+#include <cstdio>
+// [0] violations, [1] line, [2] index, [3] bound of the first one (read by the host)
+static __device__ long long g_swb_chk[4];
+static __device__ __noinline__ long long swb_chk_fail(long long i, long long n, int line) {
+  if (atomicAdd((unsigned long long*)&g_swb_chk[0], 1ULL) == 0) {
+    g_swb_chk[1] = line;
+    g_swb_chk[2] = i;
+    g_swb_chk[3] = n;
+  }
+  printf("SWB_CHECK line %d: index %lld outside [0, %lld) block %d thread %d\n", line, i, n,
+         (int)blockIdx.x, (int)threadIdx.x);
+  return 0;
+}
+#define SWB_IX(i, n)                                                              \
+  ((((long long)(i)) >= 0 && ((long long)(i)) < (long long)(n)) ? (long long)(i)  \
+                                                              : swb_chk_fail((i), (n), __LINE__))
+#else
+#define SWB_IX(i, n) (i)
+#endif
+
 namespace swb {
 
 constexpr int kTrackNone = 0;
@@ -93,6 +118,8 @@ struct JobDev {
   int32_t pad5;
 };
 
+static_assert(sizeof(JobDev) % 16 == 0, "JobDev arrays are staged next to int4 data");
+
 struct PassParams {
   const JobDev* jobs;
   int32_t njobs;
@@ -112,7 +139,28 @@ struct PassParams {
   int32_t chunk;            // > 0: CTA claims `chunk` consecutive strips (item_map: job, first)
   int32_t big;              // substitution table mode (tab) instead of tlo/thi
   const int32_t* tab;       // 32 x 33 table, device (big schemes)
+  unsigned long long launch_id;   // diagnostics: context launch counter at this launch
+  unsigned long long* claim_log;  // diagnostics ring (claim_log in swb_kernels.cuh) or null
+  unsigned long long* strip_dbg;  // per strip (item_base + s) 8 words: ranges, exit,
+                                  // block counts, live input (swb_debug_strips)
 };
+
+// Diagnostics log (swb_debug_claims): a monotonic ring over all launches of a
+// context; entries (launch id, kind | sm | cta | warp, value, globaltimer).
+__device__ __forceinline__ void claim_log(const PassParams& P, int kind, unsigned long long v) {
+  if (!P.claim_log) return;
+  const unsigned long long k = atomicAdd(P.claim_log, 1ULL) & 4095ULL;
+  unsigned smid;
+  asm("mov.u32 %0, %%smid;" : "=r"(smid));
+  unsigned long long g;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+  unsigned long long* e = P.claim_log + 8 + 4 * k;
+  e[0] = P.launch_id;
+  e[1] = ((unsigned long long)kind << 56) | ((unsigned long long)smid << 40) |
+         ((unsigned long long)blockIdx.x << 8) | (threadIdx.x >> 5);
+  e[2] = v;
+  e[3] = g;
+}
 
 // Work item -> (job, strip).  Multi-job launches claim strips strip-major
 // across jobs (item_map) so that every pass of a level advances together and
@@ -258,7 +306,7 @@ __device__ __forceinline__ void bw_flush(const JobDev& J, const BoundWriter& w, 
                                          long long v, int lane) {
   if (t < 0) return;
   const int rt = w.rt_lo + lane;
-  if (rt <= w.rt_hi) atomicMax(J.bmap_out + (long long)rt * J.map_nc + t, bound_enc(v));
+  if (rt <= w.rt_hi) atomicMax(J.bmap_out + SWB_IX((long long)rt * J.map_nc + SWB_IX(t, J.map_nc), (long long)J.map_nr * J.map_nc), bound_enc(v));
 }
 
 __device__ __forceinline__ void bw_add(const JobDev& J, BoundWriter& w, int ta, int tb,
@@ -288,7 +336,7 @@ __device__ __forceinline__ void bw_add(const JobDev& J, BoundWriter& w, int ta, 
 __device__ __forceinline__ void live_record(const JobDev& J, int rt_lo, int rt_hi, int c_lo,
                                             int c_hi) {
   for (int rt = rt_lo; rt <= rt_hi; ++rt) {
-    int4* e = J.bmap_live + rt;
+    int4* e = J.bmap_live + SWB_IX(rt, J.map_nr);
     atomicMax(&e->z, 1);
     if (c_lo <= c_hi) {
       int fa = J.map_c0 + J.map_cdir * c_lo, fb = J.map_c0 + J.map_cdir * c_hi;
@@ -308,7 +356,7 @@ __device__ __forceinline__ void live_record(const JobDev& J, int rt_lo, int rt_h
 __device__ __forceinline__ bool map_unknown(const JobDev& J, int raw, int rt, int ct) {
   if (raw >= 0) return false;
   if (!J.rmap_live) return true;
-  const int4 e = J.rmap_live[rt];
+  const int4 e = J.rmap_live[SWB_IX(rt, J.map_nr)];
   if (!e.z) return true;
   const int lo = -e.x - 1, hi = e.y;
   const int t0 = ct << kTileShift, t1 = t0 + (1 << kTileShift) - 1;
@@ -339,7 +387,7 @@ __device__ __forceinline__ long long br_get(const JobDev& J, BoundReader& r, int
   bool unknown = false;
   if (lane < n) {
     const int rt = r.rt_lo + lane / nct, ct = ta + lane % nct;
-    m = __ldcg(J.bmap_in + (long long)rt * J.map_nc + ct);
+    m = __ldcg(J.bmap_in + SWB_IX((long long)SWB_IX(rt, J.map_nr) * J.map_nc + SWB_IX(ct, J.map_nc), (long long)J.map_nr * J.map_nc));
     if (m < 0) {
       unknown = !J.bin_rev || map_unknown(J, m, rt, ct);
       if (!unknown) m = 0;  // swept fill
@@ -416,8 +464,8 @@ __device__ __forceinline__ void static_range(const JobDev& J, int s, int& cb, in
     if (ct <= ct_hi) {
       for (int rt = rt_lo; rt <= rt_hi; ++rt) {
         const long long k = (long long)rt * J.map_nc + ct;
-        const int a = __ldcg(J.rmap_fwd + k);
-        int b = __ldcg(J.rmap_rev + k);
+        const int a = __ldcg(J.rmap_fwd + SWB_IX(k, (long long)J.map_nr * J.map_nc));
+        int b = __ldcg(J.rmap_rev + SWB_IX(k, (long long)J.map_nr * J.map_nc));
         if (b < 0 && !map_unknown(J, b, rt, ct)) b = 0;  // swept fill
         if (a < 0 || b < 0 ||
             (long long)a + b - 2 * kBoundEnc + J.range_offset >= (long long)J.prune_target)
@@ -483,6 +531,17 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
   const int* __restrict__ tab_s = reinterpret_cast<const int*>(tlo_s);  // BIG: the table
   const JobDev J = Jg;
   const int lane = threadIdx.x & 31;
+  if (lane == 0) {
+    // diagnostics: who ran the strip, how often, when
+    unsigned long long* d = P.strip_dbg + 8 * (J.item_base + s);
+    d[4] = P.launch_id;  // which launch ran it
+    unsigned smid;
+    asm("mov.u32 %0, %%smid;" : "=r"(smid));
+    d[5] = ((unsigned long long)smid << 32) | ((unsigned long long)blockIdx.x << 8) | (threadIdx.x >> 5);
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    d[6] = g;
+  }
   const int goe = P.goe, ge = P.ge;
   const int go = goe - ge;
   const int n1 = J.n1, n2 = J.n2;
@@ -500,9 +559,10 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     static_range<R>(J, s, cb, ce);
     if (s > 0) static_range<R>(J, s - 1, cbp, cep);
   }
+  const int cb0 = cb;
   const int2* __restrict__ inbuf = J.buf[(s + 1) & 1];  // written by strip s-1
   int2* __restrict__ outbuf = J.buf[s & 1];
-  int32_t* my_progress = J.progress + s;
+  int32_t* my_progress = J.progress + SWB_IX(s, J.nstrips);
   const int32_t* up_progress = s > 0 ? J.progress + (s - 1) : nullptr;
   // multi-GPU row slab: strip 0 consumes the slab above (another GPU), the
   // last strip produces into the slab below (peer memory); sys-scope ordering
@@ -540,15 +600,15 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     unsigned ns = 32;
     for (;;) {
       const int p0 = ld_relaxed(up_progress);
-      if (p0 >= cep || ld_relaxed(&J.alive[s - 1].x) > 0) {
+      if (p0 >= cep || ld_relaxed(&J.alive[SWB_IX(s - 1, J.nstrips)].x) > 0) {
         const int p = ld_acquire(up_progress);
-        const int ax = ld_relaxed(&J.alive[s - 1].x);
+        const int ax = ld_relaxed(&J.alive[SWB_IX(s - 1, J.nstrips)].x);
         if (ax > 0) {
           alo_p = ax - 1;
           break;
         }
         if (p >= cep) {
-          const int ay = ld_relaxed(&J.alive[s - 1].y);
+          const int ay = ld_relaxed(&J.alive[SWB_IX(s - 1, J.nstrips)].y);
           alo_p = 0x7fffffff;
           if (ay > 0) ahi_p = ay - 1;
           break;
@@ -558,6 +618,10 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       const unsigned cap = (P.chain_wait && p0 == 0) ? kFarWaitCapNs : kWaitCapNs;
       ns = ns < cap ? ns * 2 : cap;
     }
+    // each lane polled on its own: agree on one start (the values are final
+    // once read, so the lanes agree anyway; the broadcast makes it explicit)
+    alo_p = __shfl_sync(0xffffffffu, alo_p, 0);
+    ahi_p = __reduce_min_sync(0xffffffffu, ahi_p);
     if (alo_p >= ahi_p || alo_p >= ce) cb = ce;
     else if (alo_p > cb) cb = alo_p;
   }
@@ -569,10 +633,19 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       live_record(J, rl, rh, 1, 0);  // covered, nothing swept
     }
     if (lane == 0) {
-      if (dyn) J.alive[s].y = cb + 1;  // no live output
+      if (dyn) J.alive[SWB_IX(s, J.nstrips)].y = cb + 1;  // no live output
       if (ext_out) st_release_sys(my_progress, 0x7fffffff);
       else st_release(my_progress, 0x7fffffff);
       J.strip_res[s] = make_int4(0, -1, -1, 0);
+      P.strip_dbg[8 * (J.item_base + s) + 0] = ((unsigned long long)(unsigned)cb0 << 32) | (unsigned)cb;
+      P.strip_dbg[8 * (J.item_base + s) + 1] = ((unsigned long long)(unsigned)ce << 32) | 0xffffffffu;
+      P.strip_dbg[8 * (J.item_base + s) + 2] = 0;
+      P.strip_dbg[8 * (J.item_base + s) + 3] = ((unsigned long long)(unsigned)alo_p << 32) | (unsigned)ahi_p;
+      {
+        unsigned long long g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        P.strip_dbg[8 * (J.item_base + s) + 7] = g;
+      }
       if (cout) {
         cout->ahi = cb + 1;
         __threadfence_block();
@@ -596,10 +669,10 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
   for (int r = 0; r < R; ++r) {
     const int i = lrow0 + r;
     if (BIG) {
-      sel[r] = (i < n1) ? (uint32_t)J.rows[(long long)i * J.rstep] : 32u;  // 32: pad, entry 0
+      sel[r] = (i < n1) ? (uint32_t)J.rows[SWB_IX((long long)i * J.rstep, (long long)n1 * J.rstep)] : 32u;  // 32: pad, entry 0
       continue;
     }
-    uint32_t a = (i < n1) ? (uint32_t)J.rows[(long long)i * J.rstep] : (uint32_t)kPadCode;
+    uint32_t a = (i < n1) ? (uint32_t)J.rows[SWB_IX((long long)i * J.rstep, (long long)n1 * J.rstep)] : (uint32_t)kPadCode;
     sel[r] = a | ((a | 8u) << 4) | ((a | 8u) << 8) | ((a | 8u) << 12);
   }
 
@@ -624,7 +697,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     wait_progress(up_progress, cb, ext_in);
     if (ext_in) (void)ld_acquire_sys(up_progress);
     else fence_acq_rel();
-    diag = __ldcg(inbuf + (cb - 1)).x;
+    diag = __ldcg(inbuf + SWB_IX(cb - 1, n2)).x;
   } else {
     diag = fillm;
   }
@@ -644,7 +717,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
 
   int out_hm = fillm, out_f = SWB_NEG32;
   int known_prog = 0, prune_seen = 0, published = 0;
-  int code_next = (cb + lane < ce) ? (int)J.cols[(long long)(cb + lane) * J.cstep] : 0;
+  int code_next = (cb + lane < ce) ? (int)J.cols[SWB_IX((long long)(cb + lane) * J.cstep, (long long)n2 * J.cstep)] : 0;
   long long pruned_blocks = 0, exec_blocks = 0;
   long long wait_cycles = 0;
   const long long t_strip0 = clock64();
@@ -675,7 +748,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       int fh = 0, ff = 0;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const int sv = BIG ? tab_s[rv.z + (int)sel[r]] : (int)prmt(tl, th, sel[r]);
+        const int sv = BIG ? tab_s[SWB_IX(rv.z + (int)sel[r], 32 * 33)] : (int)prmt(tl, th, sel[r]);
         const int h2 = LOCAL ? __viaddmax_s32_relu(d, sv, E[r]) : __viaddmax_s32(d, sv, E[r]);
         fv = vmaxadd(fv, -ge, hab);
         const int h2m = h2 - goe;
@@ -713,8 +786,8 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
         }
       }
       if (FINAL && lane == lstar) {
-        J.fin_h[col] = fh + goe;
-        J.fin_f[col] = ff;
+        J.fin_h[SWB_IX(col, n2)] = fh + goe;
+        J.fin_f[SWB_IX(col, n2)] = ff;
       }
       if (lane == 31) sm->out[k] = make_int2(out_hm, out_f);
     } else {
@@ -735,7 +808,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       exited = true;
       exit_col = s0;
       if (lane == 0) {
-        J.alive[s].y = (s0 - 31 > cb ? s0 - 31 : cb) + 1;
+        J.alive[SWB_IX(s, J.nstrips)].y = (s0 - 31 > cb ? s0 - 31 : cb) + 1;
         if (cout) cout->ahi = (s0 - 31 > cb ? s0 - 31 : cb) + 1;
       }
       break;
@@ -750,7 +823,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       const int pb_now = (LOCAL && J.prune == 1) ? ld_relaxed(J.prune_best) : 0;
       {
         const int cn = c + 32;
-        code_next = (cn < ce) ? (int)J.cols[(long long)cn * J.cstep] : 0;
+        code_next = (cn < ce) ? (int)J.cols[SWB_IX((long long)cn * J.cstep, (long long)n2 * J.cstep)] : 0;
       }
       if (!first && s0 < cep && s0 + 32 > cbp) {
         const int need = (s0 + 32 < cep) ? s0 + 32 : cep;
@@ -777,7 +850,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a1));
           gw += a1 - a0;
           if (dyn && ahi_p == 0x7fffffff) {
-            const int ay = ld_relaxed(&J.alive[s - 1].y);
+            const int ay = ld_relaxed(&J.alive[SWB_IX(s - 1, J.nstrips)].y);
             if (ay > 0) ahi_p = ay - 1;
           }
         } else if (known_prog < need) {
@@ -792,7 +865,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
           }
           known_prog = ext_in ? ld_acquire_sys(up_progress) : ld_acquire(up_progress);
           if (dyn && ahi_p == 0x7fffffff) {
-            const int ay = ld_relaxed(&J.alive[s - 1].y);
+            const int ay = ld_relaxed(&J.alive[SWB_IX(s - 1, J.nstrips)].y);
             if (ay > 0) ahi_p = ay - 1;
           }
         }
@@ -809,10 +882,10 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
             __threadfence_block();
             if (c < cin->prog - 96) {  // slot may have been reused: global row buffer
               if (ld_acquire(up_progress) <= c) wait_acquire(up_progress, c + 1);
-              v = __ldcg(inbuf + c);
+              v = __ldcg(inbuf + SWB_IX(c, n2));
             }
           } else {
-            v = __ldcg(inbuf + c);
+            v = __ldcg(inbuf + SWB_IX(c, n2));
           }
           th = v.x;
           tf = v.y;
@@ -820,11 +893,19 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
           th = fillm;
           tf = SWB_NEG32;
         }
-        if (BIG) sm->ring[c & 63] = make_int4(th, tf, code * 33, 0);
-        else sm->ring[c & 63] = make_int4(th, tf, (int)tlo_s[code], (int)thi_s[code]);
+        if (BIG) sm->ring[c & 63] = make_int4(th, tf, (int)SWB_IX(code, 32) * 33, 0);
+        else sm->ring[c & 63] = make_int4(th, tf, (int)tlo_s[SWB_IX(code, 8)], (int)thi_s[SWB_IX(code, 8)]);
       }
-      prune_seen = pb_now;
-      __syncwarp();
+      // Everything that steers control flow around the warp-synchronous steps
+      // must be warp-uniform: every lane loaded the running best and the
+      // producer's live end on its own, at slightly different times, and a
+      // lane that skipped or left early while the others ran the block would
+      // pair its shuffles with theirs (shfl.sync matches any shfl.sync of the
+      // same mask).  Lane 0's running best is as stale-safe as any; a known
+      // live end is final, so the minimum over lanes adopts it.
+      prune_seen = __shfl_sync(0xffffffffu, pb_now, 0);
+      if (dyn) ahi_p = __reduce_min_sync(0xffffffffu, ahi_p);
+      __syncwarp();  // ring stores visible to the steps
     }
     const bool steady = (s0 - 31 >= cb) && (s0 + 32 <= ce);
     // A restricted pass may also skip its ramp blocks: lanes that have not
@@ -972,21 +1053,21 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
         const int hi = s0 + 1 < ce ? s0 + 1 : ce;
         if (hi > cb && known_prog2 < hi) {
           if (P.chain_wait) {
-            known_prog2 = wait_acquire(J.progress + (s - 2), hi);
+            known_prog2 = wait_acquire(J.progress + SWB_IX(s - 2, J.nstrips), hi);
           } else {
             if (ld_relaxed(J.progress + (s - 2)) < hi) wait_progress(J.progress + (s - 2), hi);
             known_prog2 = ld_acquire(J.progress + (s - 2));
           }
         }
       }
-      if (c >= cb && c < ce) __stcg(outbuf + c, sm->out[lane]);
+      if (c >= cb && c < ce) __stcg(outbuf + SWB_IX(c, n2), sm->out[lane]);
       if (dyn && !lo_set) {
         // first live output: consumers start there (ordered by the release below)
         const unsigned m = __ballot_sync(0xffffffffu, c >= cb && c < ce &&
                                                           sm->out[lane].x > -(1 << 29));
         if (m) {
           lo_set = true;
-          if (lane == 0) J.alive[s].x = s0 - 31 + __ffs(m);  // (lo + 1)
+          if (lane == 0) J.alive[SWB_IX(s, J.nstrips)].x = s0 - 31 + __ffs(m);  // (lo + 1)
         }
       }
       if (ext_out) __threadfence_system();
@@ -1031,7 +1112,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     live_record(J, bw.rt_lo, bw.rt_hi, cb, exited ? exit_col - 1 : ce - 1);
   // done: consumers need columns < their own end, strip s+2 needs "finished"
   if (lane == 0) {
-    if (dyn && !exited) J.alive[s].y = ce + 1;
+    if (dyn && !exited) J.alive[SWB_IX(s, J.nstrips)].y = ce + 1;
     if (ext_out) st_release_sys(my_progress, 0x7fffffff);
     else st_release(my_progress, 0x7fffffff);
     if (cout) {
@@ -1067,7 +1148,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
         jj = oj;
       }
     }
-    if (lane == 0) J.strip_res[s] = make_int4(b, ii, jj, ii >= 0 ? 1 : 0);
+    if (lane == 0) J.strip_res[SWB_IX(s, J.nstrips)] = make_int4(b, ii, jj, ii >= 0 ? 1 : 0);
   } else if (lane == 0) {
     J.strip_res[s] = make_int4(0, -1, -1, 0);
   }
@@ -1085,6 +1166,11 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
     J.strip_times[3 * s + 0] = g0;
     J.strip_times[3 * s + 1] = g1;
+    P.strip_dbg[8 * (J.item_base + s) + 0] = ((unsigned long long)(unsigned)cb0 << 32) | (unsigned)cb;
+    P.strip_dbg[8 * (J.item_base + s) + 1] = ((unsigned long long)(unsigned)ce << 32) | (unsigned)(exited ? exit_col : -1);
+    P.strip_dbg[8 * (J.item_base + s) + 2] = ((unsigned long long)exec_blocks << 32) | (unsigned long long)pruned_blocks;
+    P.strip_dbg[8 * (J.item_base + s) + 3] = ((unsigned long long)(unsigned)alo_p << 32) | (unsigned)ahi_p;
+    P.strip_dbg[8 * (J.item_base + s) + 7] = g1;
     // proto 9 (diagnostics): the strip's final column range instead of the wait time
     J.strip_times[3 * s + 2] =
         P.proto == 9 ? (((unsigned long long)(unsigned)cb << 32) | (unsigned)ce) : gw;
@@ -1183,9 +1269,14 @@ __global__ void __launch_bounds__(256) pass_kernel(const PassParams P) {
     }
     return;
   }
+  if (P.claim_log && lane == 0) {
+    claim_log(P, 2, (unsigned long long)ld_relaxed((const int32_t*)P.claim));
+    claim_log(P, 3, (unsigned long long)(unsigned)ld_relaxed(P.jobs[0].progress));
+  }
   for (;;) {
     long long item = 0;
     if (lane == 0) item = (long long)atomicAdd(P.claim, 1ULL);
+    if (lane == 0) claim_log(P, 1, (unsigned long long)item);
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item >= P.total_items) break;
     run_item<R, LOCAL, TRACK, BIG>(P, item, sm, tlo_s, thi_s);

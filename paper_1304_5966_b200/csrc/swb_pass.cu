@@ -2,6 +2,8 @@
 // launch per (recurrence, tracking, rows-per-lane) class -> PassResult.
 // Replaces WavefrontEngine.run_wavefront (engine.py:188-282).
 #include <algorithm>
+#include <chrono>
+#include <thread>
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -338,6 +340,38 @@ struct Arena {
 
 }  // namespace
 
+// Watchdog dump: claim counter, per-strip progress / live range / diagnostics
+// record of a launch that is still running, read on a second stream.
+static void swb_watchdog_dump(swb_ctx* ctx, const unsigned long long* d_claim, const int32_t* d_prog,
+                              const int2* d_alive, const unsigned long long* d_sdbg,
+                              long long strips, long long items) {
+  cudaStream_t st;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return;
+  const long long n = std::min<long long>(strips, 4096);
+  unsigned long long* h = nullptr;
+  if (cudaMallocHost(&h, 8 * (1 + n + n + 8 * n)) != cudaSuccess) return;
+  unsigned long long* hc = h;
+  int32_t* hp = reinterpret_cast<int32_t*>(h + 1);
+  int2* ha = reinterpret_cast<int2*>(h + 1 + n);
+  unsigned long long* hd = h + 1 + 2 * n;
+  cudaMemcpyAsync(hc, d_claim, 8, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(hp, d_prog, 4 * n, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(ha, d_alive, 8 * n, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(hd, d_sdbg, 64 * n, cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  fprintf(stderr, "[swb watchdog] launch %lld: claim %llu of %lld items, %lld strips\n",
+          (long long)ctx->launches, hc[0], items, strips);
+  for (long long q = 0; q < n; ++q)
+    fprintf(stderr,
+            "[swb watchdog] strip %lld: progress %d alive (%d,%d) cb %d/%d ce %d exit %d "
+            "exec %llu skip %llu live (%d,%d) launch %llu sm %llu cta %llu warp %llu t0 %llu\n",
+            q, hp[q], ha[q].x, ha[q].y, (int)(hd[8 * q] >> 32), (int)(unsigned)hd[8 * q],
+            (int)(hd[8 * q + 1] >> 32), (int)(unsigned)hd[8 * q + 1], hd[8 * q + 2] >> 32,
+            hd[8 * q + 2] & 0xffffffffu, (int)(hd[8 * q + 3] >> 32), (int)(unsigned)hd[8 * q + 3],
+            hd[8 * q + 4], hd[8 * q + 5] >> 32, (hd[8 * q + 5] >> 8) & 0xffffff, hd[8 * q + 5] & 0xff, hd[8 * q + 6]);
+  fflush(stderr);
+}
+
 int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs,
                    double* kernel_ms_total) {
   if (kernel_ms_total) *kernel_ms_total = 0.0;
@@ -413,6 +447,25 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
       return swb_fail(SWB_EINVAL,
                       "row slab of %d rows feeding another slab must be a multiple of 32 x %d "
                       "(set rows_per_lane)", r.n1, r.R);
+  // Final rows the caller did not place get their own buffer for the whole
+  // call: the per-group arena below is reused by the next launch group, and
+  // the rows are copied to the host only after every group has run.
+  {
+    long long fcols = 0;
+    for (const PassReq& r : reqs)
+      if (r.want_final && r.fin_h_dev == nullptr) fcols += 2LL * r.n2 + 64;
+    if (fcols > 0) {
+      int32_t* f = (int32_t*)swb_scratch(ctx->pass_finals, sizeof(int32_t) * (size_t)fcols);
+      if (!f) return swb_fail(SWB_ECUDA, "out of device memory for final rows");
+      long long o = 0;
+      for (PassReq& r : reqs)
+        if (r.want_final && r.fin_h_dev == nullptr) {
+          r.fin_h_dev = f + o;
+          r.fin_f_dev = f + o + r.n2;
+          o += ((2LL * r.n2 + 63) / 64) * 64;
+        }
+    }
+  }
   auto key = [&](int q) { return cls(q) * 1000 + reqs[q].R; };
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return key(a) < key(b); });
 
@@ -425,20 +478,19 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     const int nj = (int)(g1 - g0);
 
     // layout
-    long long total_strips = 0, total_cols = 0, final_cols = 0;
+    long long total_strips = 0, total_cols = 0;
     for (size_t t = g0; t < g1; ++t) {
       PassReq& r = reqs[order[t]];
       const long long rows_item = (r.x2 ? 64LL : 32LL) * R;
       r.nstrips = (int)((r.n1 + rows_item - 1) / rows_item);
       total_strips += r.nstrips;
       total_cols += r.n2;
-      if (r.want_final && r.fin_h_dev == nullptr) final_cols += r.n2;
     }
     size_t bytes = 256 * 8 + sizeof(JobDev) * nj + sizeof(int32_t) * total_strips +
                    sizeof(int2) * total_strips + 256 + sizeof(int32_t) * 32 * kTabStride + 256 +
                    sizeof(unsigned long long) * 5 * nj + sizeof(int32_t) * nj + 64 +
                    sizeof(int4) * total_strips + 24 * total_strips + sizeof(int2) * 2 * total_cols +
-                   sizeof(int32_t) * 2 * final_cols + 4096 + 256 * 8 * (size_t)nj +
+                   4096 + 256 * 8 * (size_t)nj +
                    sizeof(int2) * total_strips + 256;
     Arena A;
     A.base = (char*)swb_scratch(ctx->rowbuf, bytes);
@@ -456,15 +508,18 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     int4* d_res = A.take<int4>(total_strips);
     unsigned long long* d_times = A.take<unsigned long long>(3 * total_strips);
     // host staging (pinned)
-    size_t hbytes = sizeof(JobDev) * nj + sizeof(int4) * total_strips +
-                    sizeof(unsigned long long) * 5 * nj + sizeof(int2) * total_strips + 1024;
+    // (every section 256-byte aligned: int4 needs 16-byte alignment on the host too)
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t h_off_res = al(sizeof(JobDev) * nj);
+    const size_t h_off_cnt = h_off_res + al(sizeof(int4) * total_strips);
+    const size_t h_off_map = h_off_cnt + al(sizeof(unsigned long long) * 5 * nj);
+    const size_t hbytes = h_off_map + al(sizeof(int2) * total_strips) + 256;
     char* hbase = (char*)swb_scratch_host(ctx->host_pinned, hbytes);
     if (!hbase) return swb_fail(SWB_ECUDA, "pinned host allocation failed");
     JobDev* h_jobs = reinterpret_cast<JobDev*>(hbase);
-    int4* h_res = reinterpret_cast<int4*>(hbase + sizeof(JobDev) * nj);
-    unsigned long long* h_cnt =
-        reinterpret_cast<unsigned long long*>(hbase + sizeof(JobDev) * nj + sizeof(int4) * total_strips);
-    int2* h_map = reinterpret_cast<int2*>(h_cnt + 5 * nj);
+    int4* h_res = reinterpret_cast<int4*>(hbase + h_off_res);
+    unsigned long long* h_cnt = reinterpret_cast<unsigned long long*>(hbase + h_off_cnt);
+    int2* h_map = reinterpret_cast<int2*>(hbase + h_off_map);
 
     long long item = 0, strip_off = 0;
     for (int t = 0; t < nj; ++t) {
@@ -509,10 +564,9 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
                                                     -(1LL << 29));
       J.alive = (r.border == SWB_BORDER_RESTRICTED && !r.ext_in && !r.ext_out && ctx->live_ranges)
                     ? d_alive + strip_off : nullptr;
-      // Early exit stays off for shared-table (BIG) passes: golden protein record 85
-      // (1171 x 144, BLOSUM62 11/1) faults in phase 2 when late start, early exit and
-      // tile bound maps combine (tools/repro_zero_protein.py)
-      J.live_mode = sc.big ? (ctx->live_ranges & 1) : ctx->live_ranges;
+      // (option live_big masks the live-range features of shared-table passes;
+      // diagnostics only since the warp-divergent early exit was fixed)
+      J.live_mode = sc.big ? (ctx->live_ranges & ctx->live_big) : ctx->live_ranges;
       J.bmap_live = (J.alive && r.bmap_live) ? r.bmap_live : nullptr;
       J.rmap_live = r.rmap_live;
       J.bin_rev = r.bin_rev;
@@ -531,15 +585,8 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
       J.counters = d_cnt + 5 * t;
       J.prune_best = d_pbest + t;
       if (r.want_final) {
-        if (r.fin_h_dev) {
-          J.fin_h = r.fin_h_dev;
-          J.fin_f = r.fin_f_dev;
-        } else {
-          J.fin_h = A.take<int32_t>(r.n2);
-          J.fin_f = A.take<int32_t>(r.n2);
-          r.fin_h_dev = J.fin_h;
-          r.fin_f_dev = J.fin_f;
-        }
+        J.fin_h = r.fin_h_dev;
+        J.fin_f = r.fin_f_dev;
       }
       r.res_offset = strip_off;
       item += r.nstrips;
@@ -611,6 +658,20 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     P.item_map = d_map;
     P.big = sc.big;
     P.tab = d_tab;
+    // diagnostics record outside the pass arena (the arena layout stays as is)
+    unsigned long long* d_sdbg =
+        (unsigned long long*)swb_scratch(ctx->dbg_buf, sizeof(unsigned long long) * 8 * total_strips);
+    if (!d_sdbg) return swb_fail(SWB_ECUDA, "out of device memory (strip diagnostics)");
+    P.strip_dbg = d_sdbg;
+    P.launch_id = (unsigned long long)ctx->launches;
+    if (ctx->claim_log_on) {
+      if (!ctx->claim_log.p) {
+        if (!swb_scratch(ctx->claim_log, 8 * (8 + 4 * 4096))) return swb_fail(SWB_ECUDA, "claim log");
+        SWB_CUDA(cudaMemsetAsync(ctx->claim_log.p, 0, 8 * (8 + 4 * 4096), ctx->stream));
+        SWB_CUDA(cudaStreamSynchronize(ctx->stream));
+      }
+      P.claim_log = (unsigned long long*)ctx->claim_log.p;
+    }
     // passes restricted to a narrow corridor are chains along the diagonal:
     // spread their strips over warps and interleave the jobs (no pairing)
     for (size_t t = g0; t < g1; ++t)
@@ -636,9 +697,52 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
                              ctx->stream));
     SWB_CUDA(cudaMemcpyAsync(h_cnt, d_cnt, sizeof(unsigned long long) * 5 * nj,
                              cudaMemcpyDeviceToHost, ctx->stream));
+    if (ctx->watchdog_ms > 0) {
+      // Watchdog (diagnostics): a launch that has not finished in time is
+      // described from a second stream while it still runs, then reported.
+      const auto t_start = std::chrono::steady_clock::now();
+      for (;;) {
+        const cudaError_t q = cudaStreamQuery(ctx->stream);
+        if (q == cudaSuccess) break;
+        if (q != cudaErrorNotReady) SWB_CUDA(q);
+        const double el = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
+                                                                    t_start).count();
+        if (el > ctx->watchdog_ms) {
+          swb_watchdog_dump(ctx, d_claim, d_prog, d_alive, d_sdbg, total_strips, P.total_items);
+          return swb_fail(SWB_ECUDA, "watchdog: pass launch (%d jobs, %lld strips) still running after %d ms",
+                          nj, total_strips, ctx->watchdog_ms);
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(200));
+      }
+    }
     SWB_CUDA(cudaStreamSynchronize(ctx->stream));
     ctx->dbg_times.resize(3 * total_strips);
     SWB_CUDA(cudaMemcpy(ctx->dbg_times.data(), d_times, 24 * total_strips, cudaMemcpyDeviceToHost));
+    ctx->dbg_strips.resize(12 * total_strips);
+    {
+      std::vector<unsigned long long> t(8 * total_strips);
+      SWB_CUDA(cudaMemcpy(t.data(), d_sdbg, 64 * total_strips, cudaMemcpyDeviceToHost));
+      for (long long q = 0; q < total_strips; ++q) {
+        for (int w = 0; w < 8; ++w) ctx->dbg_strips[12 * q + w] = (long long)t[8 * q + w];
+        ctx->dbg_strips[12 * q + 8] = h_res[q].x;
+        ctx->dbg_strips[12 * q + 9] = h_res[q].y;
+        ctx->dbg_strips[12 * q + 10] = h_res[q].z;
+        ctx->dbg_strips[12 * q + 11] = h_res[q].w;
+      }
+    }
+#ifdef SWB_CHECKED
+    {
+      long long chk[4];
+      SWB_CUDA(cudaMemcpyFromSymbol(chk, g_swb_chk, sizeof(chk)));
+      if (chk[0]) {
+        const long long zero[4] = {0, 0, 0, 0};
+        SWB_CUDA(cudaMemcpyToSymbol(g_swb_chk, zero, sizeof(zero)));
+        return swb_fail(SWB_ECUDA,
+                        "device bounds check: %lld bad indices, first at swb_kernels.cuh:%lld "
+                        "(index %lld outside [0, %lld))", chk[0], chk[1], chk[2], chk[3]);
+      }
+    }
+#endif
     float ms = 0.f;
     SWB_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
     ctx->last_kernel_ms = ms;
@@ -820,6 +924,8 @@ extern "C" int64_t swb_get_option(swb_ctx* ctx, const char* name) {
   if (!strcmp(name, "chain_wait")) return ctx->chain_wait;
   if (!strcmp(name, "chain_cta")) return ctx->chain_cta;
   if (!strcmp(name, "live_ranges")) return ctx->live_ranges;
+  if (!strcmp(name, "live_big")) return ctx->live_big;
+  if (!strcmp(name, "watchdog_ms")) return ctx->watchdog_ms;
   if (!strcmp(name, "p2_R")) return ctx->p2_R;
   if (!strcmp(name, "mm_prune")) return ctx->mm_prune;
   if (!strcmp(name, "claim_mode")) return ctx->claim_mode;
@@ -868,6 +974,18 @@ extern "C" int32_t swb_set_option(swb_ctx* ctx, const char* name, int64_t value)
   }
   if (!strcmp(name, "p2_R")) {
     ctx->p2_R = (int)value;
+    return SWB_OK;
+  }
+  if (!strcmp(name, "claim_log")) {
+    ctx->claim_log_on = (int)value;
+    return SWB_OK;
+  }
+  if (!strcmp(name, "watchdog_ms")) {
+    ctx->watchdog_ms = (int)value;
+    return SWB_OK;
+  }
+  if (!strcmp(name, "live_big")) {
+    ctx->live_big = (int)value;
     return SWB_OK;
   }
   if (!strcmp(name, "live_ranges")) {
@@ -1067,6 +1185,23 @@ extern "C" int32_t swb_debug_times(swb_ctx* ctx, int64_t* out, int32_t n) {
   if (!ctx || !out) return swb_fail(SWB_EINVAL, "bad arguments");
   int32_t m = (int32_t)ctx->dbg_times.size();
   for (int32_t q = 0; q < n && q < m; ++q) out[q] = (int64_t)ctx->dbg_times[q];
+  return m;
+}
+
+extern "C" int32_t swb_debug_strips(swb_ctx* ctx, int64_t* out, int32_t n) {
+  if (!ctx) return swb_fail(SWB_EINVAL, "bad arguments");
+  const int32_t m = (int32_t)ctx->dbg_strips.size();
+  for (int32_t q = 0; out && q < n && q < m; ++q) out[q] = ctx->dbg_strips[q];
+  return m;
+}
+
+extern "C" int32_t swb_debug_claims(swb_ctx* ctx, int64_t* out, int32_t n) {
+  if (!ctx) return swb_fail(SWB_EINVAL, "bad arguments");
+  const int32_t m = 8 + 4 * 4096;
+  if (!ctx->claim_log.p || !out) return ctx->claim_log.p ? m : 0;
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return swb_fail(SWB_ECUDA, "sync");
+  if (cudaMemcpy(out, ctx->claim_log.p, 8 * (size_t)std::min(n, m), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return swb_fail(SWB_ECUDA, "copy");
   return m;
 }
 

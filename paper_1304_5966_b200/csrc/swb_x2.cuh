@@ -298,7 +298,8 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
       sm->prof[lane] = p1;
       sm->prof[32 + lane] = p2;
       sm->prof[64 + lane] = c < n2 ? tw_s[code] : 0u;
-      prune_seen = pb_now;
+      // warp-uniform: it steers skip / tracking around the shuffling steps
+      prune_seen = __shfl_sync(0xffffffffu, pb_now, 0);
     }
 
     // (1b) re-base: warp maximum over the state and the incoming top row
@@ -557,6 +558,10 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
     J.strip_times[3 * s + 0] = g0;
     J.strip_times[3 * s + 1] = g1;
+    P.strip_dbg[8 * (J.item_base + s) + 0] = (unsigned)n2;
+    P.strip_dbg[8 * (J.item_base + s) + 1] = ((unsigned long long)(unsigned)n2 << 32) | 0xffffffffu;
+    P.strip_dbg[8 * (J.item_base + s) + 2] = ((unsigned long long)exec_blocks << 32) | (unsigned long long)pruned_blocks;
+    P.strip_dbg[8 * (J.item_base + s) + 3] = 0;
     J.strip_times[3 * s + 2] = P.proto == 10 ? g_diag : gw;  // proto 10: diagonal entry time
   }
 }

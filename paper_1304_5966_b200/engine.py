@@ -167,6 +167,49 @@ class DeviceContext:
         m = self.lib.swb_debug_times(self.ptr, out.ctypes.data, n)
         return out[:max(0, min(m, n))].reshape(-1, 3)
 
+    def debug_strips(self) -> np.ndarray:
+        """Per-strip record of the last pass launch (include/swb.h
+        swb_debug_strips): columns cb_static, cb_start, ce, exit_col, executed,
+        skipped, live_lo, live_hi, launch, sm, cta, warp, start_ns, end_ns, key, i, j, has."""
+        m = int(self.lib.swb_debug_strips(self.ptr, None, 0))
+        raw = np.zeros(max(m, 0), dtype=np.int64)
+        if m > 0:
+            self.lib.swb_debug_strips(self.ptr, raw.ctypes.data, m)
+        raw = raw.reshape(-1, 12)
+        hi = (raw[:, :4] >> 32).astype(np.int32).astype(np.int64)
+        lo = (raw[:, :4] & 0xffffffff).astype(np.uint32).view(np.int32).astype(np.int64)
+        out = np.empty((raw.shape[0], 18), dtype=np.int64)
+        out[:, 0:8:2] = hi
+        out[:, 1:8:2] = lo
+        out[:, 8] = raw[:, 4]
+        out[:, 9] = raw[:, 5] >> 32
+        out[:, 10] = (raw[:, 5] >> 8) & 0xffffff
+        out[:, 11] = raw[:, 5] & 0xff
+        out[:, 12] = raw[:, 6]
+        out[:, 13] = raw[:, 7]
+        out[:, 14:] = raw[:, 8:]
+        return out
+
+    def debug_claims(self, launch: int | None = None) -> np.ndarray:
+        """Claim log entries (launch, kind, sm, cta, warp, value, ns), oldest
+        first, optionally of one launch (include/swb.h swb_debug_claims)."""
+        m = int(self.lib.swb_debug_claims(self.ptr, None, 0))
+        if m <= 0:
+            return np.zeros((0, 7), dtype=np.int64)
+        raw = np.zeros(m, dtype=np.int64)
+        self.lib.swb_debug_claims(self.ptr, raw.ctypes.data, m)
+        total = int(raw[0])
+        ent = raw[8:].reshape(-1, 4)
+        idx = np.arange(max(0, total - 4096), total) % 4096
+        ent = ent[idx]
+        w = ent[:, 1].view(np.uint64)
+        out = np.stack([ent[:, 0], (w >> 56).astype(np.int64), ((w >> 40) & 0xffff).astype(np.int64),
+                        ((w >> 8) & 0xffffffff).astype(np.int64), (w & 0xff).astype(np.int64),
+                        ent[:, 2], ent[:, 3]], axis=1)
+        if launch is not None:
+            out = out[out[:, 0] == launch]
+        return out
+
     @property
     def launch_count(self) -> int:
         return int(self.lib.swb_launch_count(self.ptr))

@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import logging
 import math
+import os
 from dataclasses import dataclass
 
 from .engine import TRACK_MAX, Session, bound_slack
@@ -84,6 +85,10 @@ def restricted_search(S: Session, rows: tuple, cols: tuple, target: int, interva
                       prune_target=target, **extra)])[0]
     if res.best_i < 0 or res.best_score != target:
         found = res.best_score if res.best_i >= 0 else "none"
+        if os.environ.get("SWB_DUMP_ON_FAIL"):  # per-strip record of the failed launch
+            print(f"restricted pass {rows} x {cols} band {interval} target {target}: "
+                  f"{res} launches {S.ctx.launch_count}\n{S.ctx.debug_strips().tolist()}\n"
+                  f"claims {S.ctx.debug_claims(S.ctx.launch_count - 1).tolist()}", flush=True)
         raise StartNotFound(f"no cell attains the known score {target} (best found: {found}); "
                             "this indicates an internal bug")
     return res.best_i, res.best_j

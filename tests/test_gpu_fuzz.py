@@ -107,15 +107,34 @@ def test_fuzz_zero_score_pairs():
 
 
 def test_protein_record_85_repeated(golden_protein):
-    """Golden protein record 85 (1171 x 144, a 12-residue local hit) once
-    faulted in phase 2 when late start, early exit and tile bound maps
-    combined on the shared-table kernel; repeated because the
-    fault was timing dependent."""
+    """Golden protein record 85 (1171 x 144, a 12-residue local hit): its
+    phase-2 pass (3 strips, 49 columns) used to fault or return a wrong start
+    after a zero-score DNA alignment had run in the same process.  Root cause
+    (DESIGN.md §7): lanes read the producer's live end at slightly different
+    times, so some lanes took the early exit while the others ran the block and
+    their shuffles paired with the exited lanes' (shfl.sync matches any
+    shfl.sync of the same mask), which ran a strip twice and corrupted its
+    values.  The sequence below is the reproducer (tools/repro_zero_protein.py
+    a1), with every live-range feature on, repeated."""
     from helpers import golden_inputs
+    from paper_1304_5966_b200.engine import get_context
+    ctx = get_context(0)
+    assert ctx.get_option("live_big") == 3 and ctx.get_option("live_ranges") == 3
+    rng = np.random.default_rng(77)
+    alpha = Alphabet.dna(wildcard=False)
+    m = np.full((4, 4), -2, dtype=np.int64)
+    m[0, 0] = 3
+    zscheme = ScoringScheme(alpha, m, 4, 1, 3)
+    for n1, n2 in ((1, 1), (37, 900)):
+        a = rng.integers(1, 4, size=n1, dtype=np.uint8)
+        b = rng.integers(0, 4, size=n2, dtype=np.uint8)
+    swb.align(Sequence.from_codes("a", a, alpha), Sequence.from_codes("b", b, alpha), zscheme)
     rec = golden_protein[85]
     s1, s2, scheme = golden_inputs(rec)
-    for _ in range(10):
+    for _ in range(30):
+        assert swb.score_only(s1, s2, scheme).score == rec["score_only"]["score"]
         summary, path = swb.align(s1, s2, scheme)
         assert summary.score == rec["align"]["score"]
         assert list(summary.start) == rec["align"]["start"]
         assert list(summary.end) == rec["align"]["end"]
+        assert swb.path_to_cigar(path) == rec["align"]["cigar"]
