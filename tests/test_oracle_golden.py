@@ -79,3 +79,31 @@ def test_oracle_prune_invariance(rng):
     q = oracle.score_only(a, b, osch, prune=False, block=(128, 128))
     assert p[:2] == q[:2]
     assert p[2].pruned > 0
+
+
+def test_scale_goldens_self_consistent():
+    """The BASELINE-scale reference records (tests/golden/make_golden_scale.py)
+    are consistent with their own inputs: the CIGAR re-scores to the score and
+    spans start..end (model.score_of_path, reference model.py:279-318)."""
+    import gzip
+    import json
+    from pathlib import Path
+
+    from bench import synthetic_pair
+    from paper_1304_5966_b200 import Alphabet, ScoringScheme, Sequence, score_of_path
+    from paper_1304_5966_b200.model import AlignmentPath, Coord, cigar_to_ops
+
+    recs = json.load(gzip.open(Path(__file__).resolve().parent / "golden" / "golden_scale.json.gz", "rt"))
+    assert {r["name"] for r in recs} >= {"C2", "C3w", "C5w", "C3w_split", "C4w"}
+    scheme = ScoringScheme.match_mismatch(Alphabet.dna(), 1, -3, 5, 2)
+    for r in recs:
+        if "cigar" not in r:
+            continue
+        a, b = synthetic_pair(r["n"], seed=r["seed"], homologous=r["homologous"])
+        if r["window"]:
+            a, b = a[:r["window"][0]], b[:r["window"][1]]
+        s1 = Sequence.from_codes("t", a, scheme.alphabet)
+        s2 = Sequence.from_codes("q", b, scheme.alphabet)
+        path = AlignmentPath(Coord(*r["start"]), cigar_to_ops(r["cigar"]))
+        assert tuple(path.end) == tuple(r["end"]), r["name"]
+        assert score_of_path(path, s1, s2, scheme) == r["score"], r["name"]
