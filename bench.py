@@ -3,6 +3,7 @@
 Default (N=1): BASELINE config C2 — synthetic 1 Mbp x 1 Mbp homologous DNA pair
 (mutate 10 %, seed 1002), match +1 / mismatch -3 / gap 5 + 2k, forward local
 score pass with endpoint (score_only).  A step is one full score pass.
+`--workload c4` runs C4 (10 Mbp x 10 Mbp unrelated, seed 1004) instead.
 
   value     GCUPS = n1*n2 / device time, inputs resident in HBM, CUDA events on
             the launching stream around each step, L2 flushed (512 MiB write)
@@ -10,10 +11,15 @@ score pass with endpoint (score_only).  A step is one full score pass.
   e2e       the same metric through the public API score_only(Sequence, ...)
             with host buffers: H2D of both sequences, device reverse copies,
             the pass and the D2H of the result inside the timed region.
-  roofline  integer/DPX issue roofline of the pass kernel: ALU-pipe instructions
-            per executed cell (packed 16x2 kernel: 5 per cell pair = 2.5; 32-bit
-            kernel: 6) against the chip DPX issue rate measured
-            live by swb_measure_int_peak.
+  parity    the step's (score, end) against the reference's own output on the
+            same pair (tests/golden/golden_scale.json.gz, made by running
+            wavealign unchanged; tests/golden/make_golden_scale.py).
+  roofline  integer/DPX roofline of the pass kernel: 8
+            algorithmic int ops per executed cell over the mean kernel time of
+            the timed steps, against the chip's DPX issue rate measured live
+            (swb_measure_int_peak; the packed 16x2 kernel does two 16-bit ops
+            per lane-op, so its peak is twice the lane-op rate).  Beside it the
+            kernel's ALU-pipe issue fraction (instructions it actually issues).
   cpu_baseline  the CPU oracle port (oracle/, C + OpenMP block wavefront, a
             restatement of the reference engine) on a bounded window of the
             same pair, all host threads.
@@ -23,9 +29,10 @@ score pass with endpoint (score_only).  A step is one full score pass.
             check, C3 5 Mbp on the GPU (CPU time extrapolated, lower bound).
 
 `--impl reference` times that CPU port alone on the same metric (rank 0 only).
-Multi-GPU (torchrun, N>1): ONE alignment of an (N x 1 Mbp) x 1 Mbp pair split
-into row slabs, one per GPU, the slab boundary rows streamed GPU to GPU over
-NVLink through CUDA-IPC peer memory (weak scaling).
+Multi-GPU (torchrun, N>1): C4 strong scaling — ONE 10 Mbp x 10 Mbp unrelated
+score pass split into N row slabs, one per GPU, the slab boundary rows
+streamed GPU to GPU over NVLink through CUDA-IPC peer memory (DESIGN.md §6);
+time = max over ranks of each rank's CUDA-event time.
 """
 from __future__ import annotations
 
@@ -45,11 +52,84 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 N_DEFAULT = 1_000_000
-# ALU-pipe instructions per cell of the recurrence:
+C4_N = 10_000_000
+# algorithmic work of the cell update in minimal DPX form
+ALG_OPS_PER_CELL = 8
+# ALU-pipe instructions the kernels issue per cell:
 #   lane32     PRMT + 4 VIADDMNMX + running max                       = 6
 #   packed16x2 PRMT + VIMNMX3 + 3 VIADDMNMX per two cells (S16x2)   = 2.5
 OPS_PER_CELL = {"lane32": 6.0, "packed16x2": 2.5}
+# 16-bit ops per lane-op: the packed kernel computes two cells per instruction
+LANES_PER_OP = {"lane32": 1, "packed16x2": 2}
 DTYPE = {"lane32": "int32", "packed16x2": "int16x2"}
+GOLDEN_SCALE = ROOT / "tests" / "golden" / "golden_scale.json.gz"
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def golden_parity(name: str, score: int, end) -> dict | None:
+    """(score, end) of this run against the reference's output on the same
+    pair (tests/golden/golden_scale.json.gz), when the golden covers it."""
+    import gzip
+    try:
+        recs = {r["name"]: r for r in json.load(gzip.open(GOLDEN_SCALE, "rt"))}
+    except (OSError, ValueError):
+        return None
+    g = recs.get(name)
+    if g is None:
+        return None
+    return {"golden": f"tests/golden/golden_scale.json.gz:{name} (reference wavealign, "
+                      f"{g['workers']} workers, {g['ref_seconds']:.0f} s)",
+            "reference": [g["score"], g["end"]], "this_run": [int(score), [int(end[0]), int(end[1])]],
+            "match": bool(g["score"] == score and list(g["end"]) == [int(end[0]), int(end[1])])}
+
+
+def roofline_of(res_kernel: str, exec_cells: int, kernel_ms_mean: float, peak: dict,
+                traffic: dict | None) -> dict:
+    """Integer roofline of the pass kernel."""
+    lane_rate = peak["viaddmnmx"] / 1e12               # lane-ops / s (all SMs, live)
+    pk = lane_rate * LANES_PER_OP[res_kernel]          # 16-bit ops count twice per lane-op
+    ach = exec_cells * ALG_OPS_PER_CELL / (kernel_ms_mean * 1e-3) / 1e12
+    issue = exec_cells * OPS_PER_CELL[res_kernel] / (kernel_ms_mean * 1e-3) / 1e12
+    out = {"bound": "int", "achieved": ach, "peak": pk, "unit": "Tops/s", "frac": ach / pk,
+           "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+           "definition": f"{ALG_OPS_PER_CELL} algorithmic int ops per executed cell (SURVEY.md "
+                         "§8(d)) / mean kernel time of the timed steps; peak = live VIADDMNMX "
+                         f"lane-op rate x {LANES_PER_OP[res_kernel]} ops per lane-op",
+           "alu_issue": {"ops_per_cell": OPS_PER_CELL[res_kernel], "achieved": issue,
+                         "peak": lane_rate, "frac": issue / lane_rate,
+                         "note": "ALU-pipe instructions the kernel's cell update issues per cell "
+                                 "(5 per packed cell pair), against the lane-op rate"},
+           "kernel": res_kernel, "cells_executed": int(exec_cells),
+           "gcups_executed": exec_cells / (kernel_ms_mean * 1e-3) / 1e9,
+           "kernel_ms_mean": kernel_ms_mean,
+           "peak_source": "live swb_measure_int_peak (VIADDMNMX issue rate, all SMs)"}
+    if traffic:
+        out["traffic_source"] = traffic.get("source")
+        if "sass_alu_ops_per_cell" in traffic:
+            out["alu_issue"]["sass_ops_per_cell"] = traffic["sass_alu_ops_per_cell"]
+            out["alu_issue"]["sass_frac"] = (exec_cells * traffic["sass_alu_ops_per_cell"] /
+                                             (kernel_ms_mean * 1e-3) / 1e12 / lane_rate)
+    return out
+
+
+def load_traffic() -> dict | None:
+    for name in ("r02_traffic.json", "r01_traffic.json"):
+        p = ROOT / "profiles" / name
+        if p.exists():
+            try:
+                return json.loads(p.read_text())
+            except (OSError, ValueError):
+                return None
+    return None
 THROTTLE_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
                  0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
                  0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
@@ -155,6 +235,7 @@ def cpu_window(a, b, target_s: float = 15.0):
     score, end, _ = oracle.score_only(a[:w], b[:w], osch, threads=threads)
     dt = time.perf_counter() - t0
     return {"value": w * w / dt / 1e9, "unit": "GCUPS", "cores": threads, "kind": "port",
+            "cpu_model": cpu_model(),
             "sample": f"score pass on the first {w} x {w} residues of the same pair "
                       f"({dt:.1f} s, score {score})"}, w, dt
 
@@ -208,10 +289,13 @@ def align_e2e(swb, scheme, cpu_gcups, with_cpu: bool):
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the CPU port of the reference path (oracle/)."""
+    """--impl reference: the CPU port of the reference path (oracle/, C +
+    OpenMP restatement of kernels.affine_block / WavefrontEngine.run_wavefront),
+    all host threads, each step a bounded square window of the same workload
+    (the full C2 pair takes ~37 min on 8 cores in the reference itself)."""
     if rank != 0:
         return 0
-    a, b = synthetic_pair(args.n, homologous=not args.unrelated)
+    a, b, wname, wdesc, _ = workload_pair(args, world)
     vals, secs = [], []
     base = None
     for it in range(args.warmup + args.steps):
@@ -224,31 +308,46 @@ def run_reference(args, rank, world):
     line = {
         "metric": "GCUPS (score pass, full-matrix cells / time)", "value": value, "unit": "GCUPS",
         "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * statistics.mean(secs), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * statistics.mean(secs), "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": f"C2 window: score pass on a square window of the "
-                               f"{args.n} x {args.n} homologous pair", "n1": args.n, "n2": args.n,
-                   "scheme": "match +1 / mismatch -3 / gap 5+2k"},
+        "config": {"workload": wdesc, "n1": int(a.size), "n2": int(b.size),
+                   "scheme": "match +1 / mismatch -3 / gap 5+2k",
+                   "sample": "square window of the pair per step (see cpu_baseline.sample)"},
         "cpu_baseline": {"value": value, "unit": "GCUPS", "cores": base["cores"], "kind": "port",
-                         "sample": base["sample"]},
+                         "cpu_model": base["cpu_model"], "sample": base["sample"]},
         "e2e": {"value": value, "unit": "GCUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
+def workload_pair(args, world: int = 1):
+    """(a, b, name, description, golden name) of the configured workload."""
+    if args.workload == "c4" or world > 1:
+        a, b = synthetic_pair(C4_N, seed=1004, homologous=False)
+        return a, b, "C4", ("C4: 10 Mbp x 10 Mbp unrelated DNA pair (seed 1004), score + endpoint "
+                            "forward pass (no pruning possible: worst-case wavefront)"), None
+    a, b = synthetic_pair(args.n, seed=1002, homologous=not args.unrelated)
+    if args.n == N_DEFAULT and not args.unrelated:
+        return a, b, "C2", ("C2: 1 Mbp x 1 Mbp homologous DNA pair (mutate 10%, seed 1002), "
+                            "score + endpoint forward pass"), "C2"
+    kind = "unrelated" if args.unrelated else "homologous"
+    return a, b, "custom", f"{a.size} x {b.size} {kind} pair, score pass", None
+
+
 def run_multi(args, rank, world, local, dist):
-    """N GPUs, one alignment: the target is N x n residues (weak scaling, n x n
-    cells per GPU), split into row slabs; GPU g streams the bottom DP row of its
-    slab into GPU g+1's boundary buffer through CUDA-IPC peer memory over
-    NVLink.  Time = max over ranks of the CUDA-event time."""
+    """N GPUs, one pass (C4 strong scaling): the 10 Mbp x 10 Mbp pair is split
+    into N row slabs of whole strips, one per GPU; GPU g streams the bottom DP
+    row of its slab into GPU g+1's boundary buffer through CUDA-IPC peer memory
+    over NVLink, inside the pass kernel.  Time = max over ranks
+    of each rank's CUDA-event time around its slab; value = all cells / time."""
     import torch
     import paper_1304_5966_b200 as swb
     from paper_1304_5966_b200.engine import Session, get_context
     from paper_1304_5966_b200.multigpu import (SLAB_ROWS_PER_LANE, SLAB_STRIP_ROWS, Boundary,
                                               ipc_import, merge_best, slab_partition, slab_spec)
-    a, b = synthetic_pair(args.n * world, seed=1002, homologous=not args.unrelated)
-    b = b[:args.n]
+    a, b, wname, wdesc, _ = workload_pair(args, world)
     scheme = swb.ScoringScheme.match_mismatch(swb.Alphabet.dna(), 1, -3, 5, 2)
     ctx = get_context(local)
     peak = ctx.measure_int_peak()
@@ -276,12 +375,13 @@ def run_multi(args, rank, world, local, dist):
     with Session(ctx, a, b, scheme) as S:
         for _ in range(args.warmup):
             step(S)
-        times, res = [], None
+        times, kms, res = [], [], None
         with ClockSampler(local) as clocks:
             l0 = ctx.launch_count
             for _ in range(args.steps):
                 res, ms = step(S)
                 times.append(ms)
+                kms.append(res.kernel_ms)
             launches = ctx.launch_count - l0
         # end to end: host codes -> device (Session upload) + pass + result D2H
         e2e_ms = []
@@ -299,33 +399,35 @@ def run_multi(args, rank, world, local, dist):
     bests = [None] * world
     dist.all_gather_object(bests, (res.best_score, res.best_i, res.best_j))
     cells_all = [None] * world
-    dist.all_gather_object(cells_all, res.cells_executed)
+    dist.all_gather_object(cells_all, (res.cells_executed, statistics.mean(kms), res.kernel))
     merged = merge_best([tuple(x) for x in bests], 1)
     cells = a.size * b.size
     value = cells * args.steps / (total_ms * 1e-3) / 1e9
     if rank == 0:
-        exec_cells = sum(cells_all)
-        achieved = exec_cells * OPS_PER_CELL[res.kernel] / (total_ms / args.steps * 1e-3) / 1e12
+        # roofline of the whole job: all ranks' executed cells over the slowest
+        # rank's mean kernel time, against N GPUs' live peak
+        exec_cells = sum(c[0] for c in cells_all)
+        kmax = max(c[1] for c in cells_all)
+        peak_n = {k: v * world for k, v in peak.items() if isinstance(v, float)}
+        roof = roofline_of(res.kernel, exec_cells, kmax, peak_n, None)
+        roof["peak_source"] += f" x {world} GPUs"
         line = {
             "metric": "GCUPS (score pass, full-matrix cells / time)", "value": value,
             "unit": "GCUPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": DTYPE[res.kernel], "data": "synthetic",
-            "config": {"workload": f"one alignment: {a.size} x {b.size} homologous pair "
-                                   f"({args.n} x {args.n} cells per GPU), score + endpoint pass",
-                       "n1": int(a.size), "n2": int(b.size), "prune": True,
-                       "parallelism": f"{world} GPUs, row slabs, boundary rows streamed over "
-                                      "NVLink (CUDA IPC peer stores)",
-                       "l2": "inputs resident; boundary rows live in L2 (see DESIGN.md §6)",
-                       "score": merged[0], "end": [merged[1] + 1, merged[2] + 1]},
+            "config": {"workload": wdesc, "n1": int(a.size), "n2": int(b.size), "prune": True,
+                       "parallelism": f"{world} GPUs, row slabs of whole 1024-row strips, boundary "
+                                      "rows streamed over NVLink (CUDA IPC peer stores from the "
+                                      "pass kernel)",
+                       "l2": "inputs (20 MB of codes) resident; the pass is compute bound",
+                       "score": merged[0], "end": [merged[1] + 1, merged[2] + 1],
+                       "slab_rows": [s.rows for s in slabs]},
             "e2e": {"value": cells * args.steps / (e2e_total * 1e-3) / 1e9, "unit": "GCUPS",
                     "h2d_bytes_per_step": int(a.size + b.size),
                     "d2h_bytes_per_step": int(16 * (me.rows // SLAB_STRIP_ROWS + 1) + 40)},
             "gpu_launches": launches, "clocks": clocks.summary(),
-            "roofline": {"bound": "int", "achieved": achieved,
-                         "peak": world * peak["viaddmnmx"] / 1e12, "unit": "Tops/s",
-                         "frac": achieved / (world * peak["viaddmnmx"] / 1e12), "traffic": None},
-            "cpu_baseline": None,
+            "roofline": roof, "cpu_baseline": None,
         }
         print(json.dumps(line), flush=True)
     if ext_out:
@@ -343,6 +445,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--workload", default="c2", choices=["c2", "c4"],
+                    help="c2 (default at N=1) or c4; N > 1 always runs C4 (strong scaling)")
     ap.add_argument("--n", type=int, default=N_DEFAULT)
     ap.add_argument("--unrelated", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -359,7 +463,8 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as tdist
-        torch.cuda.set_device(local)
+        if args.impl == "native":
+            torch.cuda.set_device(local)
         tdist.init_process_group("nccl" if args.impl == "native" else "gloo")
         dist = tdist
     if args.impl == "reference":
@@ -375,27 +480,20 @@ def main():
     import paper_1304_5966_b200 as swb
     from paper_1304_5966_b200.engine import TRACK_MIN, Session, get_context
 
-    a, b = synthetic_pair(args.n, seed=1002 + rank, homologous=not args.unrelated)
+    a, b, wname, wdesc, gname = workload_pair(args)
     scheme = swb.ScoringScheme.match_mismatch(swb.Alphabet.dna(), 1, -3, 5, 2)
-    ctx = get_context(0 if world == 1 else local)
+    ctx = get_context(0)
     peak = ctx.measure_int_peak()
     cells = a.size * b.size
 
-    def barrier():
-        if dist is not None:
-            import torch
-            torch.cuda.synchronize()
-            dist.barrier()
-
     # -- device-resident value -------------------------------------------------
-    step_ms, res = [], None
+    step_ms, kernel_ms, res = [], [], None
     launches = 0
     with Session(ctx, a, b, scheme) as S:
         spec = [dict(rows=(0, S.n1, 0), cols=(0, S.n2, 0), border="local", clamp=True,
                      track=TRACK_MIN, prune=True)]
         for _ in range(args.warmup):
             S.run(spec)
-        barrier()
         with ClockSampler(local) as clocks:
             l0 = ctx.launch_count
             for _ in range(args.steps):
@@ -403,91 +501,58 @@ def main():
                 ctx.timer_start()
                 res = S.run(spec)[0]
                 step_ms.append(ctx.timer_stop())
+                kernel_ms.append(res.kernel_ms)
             launches = ctx.launch_count - l0
-        barrier()
-    kernel_ms = res.kernel_ms
     total_ms = sum(step_ms)
-    if dist is not None:
-        import torch
-        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    value = world * cells * args.steps / (total_ms * 1e-3) / 1e9
+    value = cells * args.steps / (total_ms * 1e-3) / 1e9
 
     # -- end to end through the public API ----------------------------------------
     s1 = swb.Sequence.from_codes("target", a, scheme.alphabet)
     s2 = swb.Sequence.from_codes("query", b, scheme.alphabet)
     swb.score_only(s1, s2, scheme)
-    barrier()
     e_ms = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
         r2 = swb.score_only(s1, s2, scheme)
         e_ms.append((time.perf_counter() - t0) * 1e3)
-    barrier()
-    e_total = sum(e_ms)
-    if dist is not None:
-        import torch
-        t = torch.tensor([e_total], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e_total = float(t.item())
-    e2e = world * cells * args.steps / (e_total * 1e-3) / 1e9
+    e2e = cells * args.steps / (sum(e_ms) * 1e-3) / 1e9
     assert (r2.score, r2.end) == (res.best_score, (res.best_i + 1, res.best_j + 1))
 
-    # -- roofline -------------------------------------------------------------------
-    exec_cells = res.cells_executed
-    opc = OPS_PER_CELL[res.kernel]
-    achieved = exec_cells * opc / (kernel_ms * 1e-3) / 1e12
-    peak_t = peak["viaddmnmx"] / 1e12
-    strips = (a.size + 1023) // 1024
-    roofline = {"bound": "int", "achieved": achieved, "peak": peak_t, "unit": "Tops/s",
-                "frac": achieved / peak_t, "traffic": None,
-                "peak_source": "live swb_measure_int_peak (VIADDMNMX issue rate, all SMs)",
-                "ops_per_cell": opc, "kernel": res.kernel, "rows_per_lane": res.rows_per_lane,
-                "cells_executed": exec_cells,
-                "gcups_executed": exec_cells / (kernel_ms * 1e-3) / 1e9,
-                "kernel_ms": kernel_ms, "pruned_fraction": res.pruned_blocks / max(1, res.total_blocks)}
-    prof = ROOT / "profiles" / "r01_traffic.json"
-    if prof.exists():
-        try:
-            roofline["traffic"] = json.loads(prof.read_text()).get("dram_bytes_per_launch")
-        except (OSError, ValueError):
-            pass
+    roofline = roofline_of(res.kernel, res.cells_executed, statistics.mean(kernel_ms), peak,
+                           load_traffic() if wname == "C2" else None)
+    roofline.update(rows_per_lane=res.rows_per_lane,
+                    pruned_fraction=res.pruned_blocks / max(1, res.total_blocks),
+                    kernel_share_of_step=statistics.mean(kernel_ms) / statistics.mean(step_ms))
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if not args.no_cpu:
         cpu, _, _ = cpu_window(a, b, target_s=args.cpu_seconds)
     align = None
-    if rank == 0 and world == 1 and not args.no_align:
+    if not args.no_align and wname == "C2":
         align = align_e2e(swb, scheme, cpu["value"] if cpu else None, not args.no_cpu)
 
-    if rank == 0:
-        line = {
-            "metric": "GCUPS (score pass, full-matrix cells / time)", "value": value,
-            "unit": "GCUPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": DTYPE[res.kernel], "data": "synthetic",
-            "config": {"workload": "C2: 1 Mbp x 1 Mbp homologous DNA pair (mutate 10%, seed 1002), "
-                                   "score + endpoint forward pass" if args.n == N_DEFAULT and
-                                   not args.unrelated else
-                                   f"{a.size} x {b.size} {'unrelated' if args.unrelated else 'homologous'} pair, score pass",
-                       "n1": int(a.size), "n2": int(b.size),
-                       "scheme": "match +1 / mismatch -3 / gap 5+2k, default ACGT+N alphabet",
-                       "prune": True, "l2": "flushed (512 MiB write) between timed steps",
-                       "parallelism": "1 GPU" if world == 1 else f"{world} replicas (one pair per GPU)",
-                       "score": res.best_score, "end": [res.best_i + 1, res.best_j + 1]},
-            "e2e": {"value": e2e, "unit": "GCUPS", "h2d_bytes_per_step": int(a.size + b.size),
-                    "d2h_bytes_per_step": int(16 * strips + 40)},
-            "gpu_launches": launches,
-            "clocks": clocks.summary(),
-            "roofline": roofline,
-            "cpu_baseline": cpu,
-            "align_e2e": align,
-            "int_peak": {k: v for k, v in peak.items() if k != "ms_last"},
-        }
-        print(json.dumps(line), flush=True)
-    if dist is not None:
-        dist.destroy_process_group()
+    line = {
+        "metric": "GCUPS (score pass, full-matrix cells / time)", "value": value,
+        "unit": "GCUPS", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": DTYPE[res.kernel], "data": "synthetic",
+        "config": {"workload": wdesc, "n1": int(a.size), "n2": int(b.size),
+                   "scheme": "match +1 / mismatch -3 / gap 5+2k, default ACGT+N alphabet",
+                   "prune": True, "l2": "flushed (512 MiB write) between timed steps",
+                   "parallelism": "1 GPU",
+                   "score": res.best_score, "end": [res.best_i + 1, res.best_j + 1]},
+        "parity": golden_parity(gname, res.best_score, (res.best_i + 1, res.best_j + 1))
+        if gname else None,
+        "e2e": {"value": e2e, "unit": "GCUPS", "h2d_bytes_per_step": int(a.size + b.size),
+                "d2h_bytes_per_step": int(16 * ((a.size + 1023) // 1024) + 40)},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "align_e2e": align,
+        "int_peak": {k: v for k, v in peak.items() if k != "ms_last"},
+    }
+    print(json.dumps(line), flush=True)
     return 0
 
 

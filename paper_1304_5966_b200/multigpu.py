@@ -157,6 +157,35 @@ def run_slabs_sequential(S, slabs: list[Slab], prune: bool = True):
             b.free()
 
 
+def run_slabs_concurrent(S, slabs: list[Slab], prune: bool = True):
+    """One-GPU emulation of N ranks running AT THE SAME TIME: every slab is a
+    job of ONE persistent launch, and slab g+1's first strip consumes slab g's
+    last strip through the same ext_in / ext_out boundary path (sys-scope
+    release / acquire, __threadfence_system) the NVLink peer stores use.  Jobs
+    are claimed job-major, so a strip only waits on an item claimed before it
+    and the launch stays deadlock-free (separate waiting launches on one GPU
+    are not: B200_PROFILING.md).  Returns the merged (score, i, j) and the
+    per-slab results."""
+    bounds = [Boundary(S.ctx, S.n2) for _ in slabs[1:]]
+    old_jm = S.ctx.get_option("job_major")
+    S.ctx.set_option("rows_per_lane", SLAB_ROWS_PER_LANE)
+    S.ctx.set_option("job_major", 1)
+    try:
+        specs = []
+        for g, slab in enumerate(slabs):
+            ext_in = (bounds[g - 1].buf, bounds[g - 1].progress) if g > 0 else None
+            ext_out = (bounds[g].buf, bounds[g].progress) if g + 1 < len(slabs) else None
+            specs.append(slab_spec(slab, S.n1, S.n2, ext_in, ext_out, prune))
+        results = S.run(specs)
+        merged = merge_best([(r.best_score, r.best_i, r.best_j) for r in results], TRACK_MIN)
+        return merged, results
+    finally:
+        S.ctx.set_option("rows_per_lane", 0)
+        S.ctx.set_option("job_major", old_jm)
+        for b in bounds:
+            b.free()
+
+
 class _DeviceRows:
     """__cuda_array_interface__ view of int32 device memory (a tile-map slice)
     so that torch / NCCL can move it without a copy."""

@@ -26,7 +26,8 @@ from bench import synthetic_pair
 import paper_1304_5966_b200 as swb
 from paper_1304_5966_b200 import AlignConfig, Sequence
 from paper_1304_5966_b200.engine import Session, get_context
-from paper_1304_5966_b200.multigpu import SLAB_STRIP_ROWS, run_slabs_sequential, slab_partition
+from paper_1304_5966_b200.multigpu import (SLAB_STRIP_ROWS, run_slabs_concurrent,
+                                          run_slabs_sequential, slab_partition)
 
 pytestmark = pytest.mark.gpu
 
@@ -77,6 +78,20 @@ def test_c2_row_slabs(c2, nslabs):
     with Session(get_context(0), a, b, SCHEME) as S:
         merged, _ = run_slabs_sequential(S, slab_partition(S.n1, nslabs, SLAB_STRIP_ROWS))
     assert (merged[0], [merged[1] + 1, merged[2] + 1]) == (g["score"], g["end"])
+
+
+@pytest.mark.parametrize("nslabs", [2, 4, 8])
+@pytest.mark.parametrize("prune", [True, False])
+def test_c2_row_slabs_concurrent(c2, nslabs, prune):
+    """The N-rank boundary protocol with every rank running at once: all slabs
+    in one launch, each consuming its predecessor through the ext path."""
+    _, _, a, b = c2
+    g = GOLDEN["C2"]
+    for _ in range(3):
+        with Session(get_context(0), a, b, SCHEME) as S:
+            merged, res = run_slabs_concurrent(S, slab_partition(S.n1, nslabs, SLAB_STRIP_ROWS), prune)
+        assert (merged[0], [merged[1] + 1, merged[2] + 1]) == (g["score"], g["end"])
+        assert all(r.kernel == "packed16x2" for r in res)
 
 
 def _check_align(name, cfg=None):
