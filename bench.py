@@ -346,7 +346,8 @@ def run_multi(args, rank, world, local, dist):
     import paper_1304_5966_b200 as swb
     from paper_1304_5966_b200.engine import Session, get_context
     from paper_1304_5966_b200.multigpu import (SLAB_ROWS_PER_LANE, SLAB_STRIP_ROWS, Boundary,
-                                              ipc_import, merge_best, slab_partition, slab_spec)
+                                              ipc_export, ipc_import, merge_best, slab_partition,
+                                              slab_spec)
     a, b, wname, wdesc, _ = workload_pair(args, world)
     scheme = swb.ScoringScheme.match_mismatch(swb.Alphabet.dna(), 1, -3, 5, 2)
     ctx = get_context(local)
@@ -355,21 +356,28 @@ def run_multi(args, rank, world, local, dist):
     slabs = slab_partition(a.size, world, SLAB_STRIP_ROWS)
     me = slabs[rank]
     inbound = Boundary(ctx, b.size) if rank > 0 else None
+    # the pass's running best, shared by all slabs: a word in rank 0's memory
+    # every rank raises with system-scope atomics over NVLink
+    best = Boundary(ctx, 1) if rank == 0 else None
     handles = [None] * world
-    dist.all_gather_object(handles, inbound.export() if inbound else None)
+    dist.all_gather_object(handles, (inbound.export() if inbound else None,
+                                     ipc_export(ctx, best.progress) if best else None))
     ext_out = None
     if rank + 1 < world:
-        hb, hp = handles[rank + 1]
+        hb, hp = handles[rank + 1][0]
         ext_out = (ipc_import(ctx, hb), ipc_import(ctx, hp))
     ext_in = (inbound.buf, inbound.progress) if inbound else None
+    shared_best = best.progress if best else ipc_import(ctx, handles[0][1])
 
     def step(S):
         if inbound:
             inbound.reset()
+        if best:
+            best.reset()
         torch.cuda.synchronize()
         dist.barrier()
         ctx.timer_start()
-        r = S.run([slab_spec(me, S.n1, S.n2, ext_in, ext_out)])[0]
+        r = S.run([slab_spec(me, S.n1, S.n2, ext_in, ext_out, True, shared_best)])[0]
         return r, ctx.timer_stop()
 
     with Session(ctx, a, b, scheme) as S:
@@ -419,7 +427,8 @@ def run_multi(args, rank, world, local, dist):
             "config": {"workload": wdesc, "n1": int(a.size), "n2": int(b.size), "prune": True,
                        "parallelism": f"{world} GPUs, row slabs of whole 1024-row strips, boundary "
                                       "rows streamed over NVLink (CUDA IPC peer stores from the "
-                                      "pass kernel)",
+                                      "pass kernel), running best shared through a system-scope "
+                                      "word in rank 0's memory",
                        "l2": "inputs (20 MB of codes) resident; the pass is compute bound",
                        "score": merged[0], "end": [merged[1] + 1, merged[2] + 1],
                        "slab_rows": [s.rows for s in slabs]},
@@ -433,9 +442,13 @@ def run_multi(args, rank, world, local, dist):
     if ext_out:
         ctx.lib.swb_ipc_close(ctx.ptr, ext_out[0])
         ctx.lib.swb_ipc_close(ctx.ptr, ext_out[1])
+    if not best:
+        ctx.lib.swb_ipc_close(ctx.ptr, shared_best)
     dist.barrier()
     if inbound:
         inbound.free()
+    if best:
+        best.free()
     return 0
 
 

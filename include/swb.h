@@ -135,6 +135,13 @@ typedef struct {
   int32_t bound_write;
   int32_t bound_read;
   int64_t bound_offset;
+  /* Running best shared between the row slabs of one pass (prune kind 1):
+   * device pointer to an int32 word, zero before the pass, that every slab
+   * reads (system scope) and raises with atomicMax — local memory on one GPU
+   * or a CUDA-IPC peer mapping across GPUs.  0: the pass keeps its own
+   * running best.  Any slab's best is a real cell score, so a shared best is
+   * as sound as the reference's barrier-refreshed one (engine.py:260-261). */
+  uint64_t shared_best;
 } swb_pass_desc;
 
 /* PassResult (engine.py:120-131) minus the final rows (written in place). */

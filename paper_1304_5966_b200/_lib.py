@@ -41,7 +41,8 @@ class PassDesc(ctypes.Structure):
                 ("corner_j", c_i64), ("ext_in_buf", ctypes.c_uint64),
                 ("ext_in_progress", ctypes.c_uint64), ("ext_out_buf", ctypes.c_uint64),
                 ("ext_out_progress", ctypes.c_uint64), ("rows_after", c_i64),
-                ("bound_write", c_i32), ("bound_read", c_i32), ("bound_offset", c_i64)]
+                ("bound_write", c_i32), ("bound_read", c_i32), ("bound_offset", c_i64),
+                ("shared_best", ctypes.c_uint64)]
 
 
 class PassOut(ctypes.Structure):

@@ -111,7 +111,7 @@ struct JobDev {
   const int32_t* rmap_rev;
   int2* alive;             // per strip (live lo + 1, live hi + 1), 0 = unset (restricted passes)
   int32_t live_mode;       // bit 0: late start, bit 1: early exit
-  int32_t pad4;
+  int32_t best_sys;        // prune_best is shared across slabs / GPUs: system-scope access
   int4* bmap_live;         // writer: per row tile (-(lo+1), hi, covered) of the columns it swept
   const int4* rmap_live;   // reader: unwritten reverse-map tiles outside that interval are fill
   int32_t bin_rev;         // bmap_in is the reverse map (rmap_live applies to it)
@@ -231,6 +231,16 @@ __device__ __forceinline__ int ld_relaxed(const int32_t* p) {
   int v;
   asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+
+// running best for pruning: per pass (gpu scope) or shared between the row
+// slabs of a pass, possibly on other GPUs (system scope, swb_pass_desc.shared_best)
+__device__ __forceinline__ int load_best(const JobDev& J) {
+  return J.best_sys ? ld_relaxed_sys(J.prune_best) : ld_relaxed(J.prune_best);
+}
+__device__ __forceinline__ void raise_best(const JobDev& J, int v) {
+  if (J.best_sys) atomicMax_system(J.prune_best, v);
+  else atomicMax(J.prune_best, v);
 }
 
 // Spin until *p >= need with exponential back-off: a waiting warp shares its
@@ -820,7 +830,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     {
       const int c = s0 + lane;
       const int code = code_next;
-      const int pb_now = (LOCAL && J.prune == 1) ? ld_relaxed(J.prune_best) : 0;
+      const int pb_now = (LOCAL && J.prune == 1 && lane == 0) ? load_best(J) : 0;
       {
         const int cn = c + 32;
         code_next = (cn < ce) ? (int)J.cols[SWB_IX((long long)cn * J.cstep, (long long)n2 * J.cstep)] : 0;
@@ -1103,7 +1113,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       const int bm = __reduce_max_sync(0xffffffffu, bkey >> 5);
       if (bm > -goe && bm + goe > published && bm + goe > prune_seen) {
         published = bm + goe;
-        if (lane == 0) atomicMax(J.prune_best, published);
+        if (lane == 0) raise_best(J, published);
       }
     }
   }

@@ -583,7 +583,8 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
       J.strip_res = d_res + strip_off;
       J.strip_times = d_times + 3 * strip_off;
       J.counters = d_cnt + 5 * t;
-      J.prune_best = d_pbest + t;
+      J.prune_best = r.shared_best ? r.shared_best : d_pbest + t;
+      J.best_sys = r.shared_best ? 1 : 0;
       if (r.want_final) {
         J.fin_h = r.fin_h_dev;
         J.fin_f = r.fin_f_dev;
@@ -1069,6 +1070,9 @@ extern "C" int32_t swb_pass(swb_ctx* ctx, const swb_scheme* scheme, const swb_pa
     if (d.rows_after < 0 || d.rows_after >= (1LL << 31))
       return swb_fail(SWB_ERANGE, "rows_after out of range");
     r.rows_after = d.rows_after;
+    r.shared_best = reinterpret_cast<int32_t*>(d.shared_best);
+    if (r.shared_best && (!r.local || d.prune != 1))
+      return swb_fail(SWB_EINVAL, "shared_best applies to local passes with running-best pruning");
     if ((r.ext_in || r.ext_out || r.row_offset) && r.has_band)
       return swb_fail(SWB_EUNSUPPORTED, "row slabs (multi-GPU) do not support a band");
     if ((r.ext_in == nullptr) != (r.ext_in_prog == nullptr) ||

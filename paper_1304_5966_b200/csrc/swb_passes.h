@@ -37,6 +37,7 @@ struct PassReq {
   int2* ext_out = nullptr;
   int32_t* ext_out_prog = nullptr;
   long long rows_after = 0;  // pass rows below this slab (prune bounds)
+  int32_t* shared_best = nullptr;  // running best shared between slabs (system scope)
   // tile bound maps
   int32_t* bmap_out = nullptr;
   const int32_t* bmap_in = nullptr;

@@ -268,7 +268,7 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     {
       const int code = code_next;
       // the running best also decides tracking, so it is kept with pruning off
-      const int pb_now = ld_relaxed(J.prune_best);
+      const int pb_now = lane == 0 ? load_best(J) : 0;
       {
         const int cn = c + 32;
         code_next = (cn < n2) ? (int)J.cols[(long long)cn * J.cstep] : 0;
@@ -504,7 +504,7 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
       const int bm = __reduce_max_sync(0xffffffffu, vA > vB ? vA : vB);
       if (bm > -goe && bm + goe > published && bm + goe > prune_seen) {
         published = bm + goe;
-        if (lane == 0) atomicMax(J.prune_best, published);
+        if (lane == 0) raise_best(J, published);
       }
     }
   }

@@ -367,7 +367,7 @@ class Session:
     def desc(self, rows: tuple, cols: tuple, border: str, clamp: bool, track: int,
              band=None, prune=False, final=None, row_offset=0, ext_in=None,
              ext_out=None, prune_target=0, corner=None, rows_after=0, bound_write=0,
-             bound_read=0, bound_offset=0) -> _lib.PassDesc:
+             bound_read=0, bound_offset=0, shared_best=0) -> _lib.PassDesc:
         """rows/cols = (offset, length, reversed) slices of seq1/seq2;
         row_offset/ext_in/ext_out describe a row slab of a multi-GPU pass
         (multigpu.py, include/swb.h)."""
@@ -392,6 +392,7 @@ class Session:
         d.rows_after = int(rows_after)
         d.bound_write, d.bound_read = int(bound_write), int(bound_read)
         d.bound_offset = int(bound_offset)
+        d.shared_best = int(shared_best or 0)
         if ext_in is not None:
             d.ext_in_buf, d.ext_in_progress = int(ext_in[0]), int(ext_in[1])
         if ext_out is not None:

@@ -126,13 +126,17 @@ def ipc_import(ctx, handle: bytes) -> int:
 
 
 def slab_spec(slab: Slab, n1: int, n2: int, ext_in: tuple[int, int] | None,
-              ext_out: tuple[int, int] | None, prune: bool = True) -> dict:
+              ext_out: tuple[int, int] | None, prune: bool = True, shared_best: int = 0) -> dict:
     """Session.run() spec of one slab of a local score pass (phase1.py:44-85).
     rows_after (the pass's rows below the slab) keeps the pruning bound of
-    phase1.py:55-59 sound for paths that continue on the GPUs below."""
+    phase1.py:55-59 sound for paths that continue on the GPUs below;
+    shared_best (a device word every slab reads and raises) gives every slab
+    the running best of the whole pass, as the reference's barrier-refreshed
+    best does for its blocks (engine.py:260-261)."""
     return dict(rows=(slab.row0, slab.rows, 0), cols=(0, n2, 0), border="local", clamp=True,
                 track=TRACK_MIN, prune=prune, row_offset=slab.row0,
-                ext_in=ext_in, ext_out=ext_out, rows_after=n1 - slab.row1)
+                ext_in=ext_in, ext_out=ext_out, rows_after=n1 - slab.row1,
+                shared_best=shared_best if prune else 0)
 
 
 def run_slabs_sequential(S, slabs: list[Slab], prune: bool = True):
@@ -157,16 +161,18 @@ def run_slabs_sequential(S, slabs: list[Slab], prune: bool = True):
             b.free()
 
 
-def run_slabs_concurrent(S, slabs: list[Slab], prune: bool = True):
+def run_slabs_concurrent(S, slabs: list[Slab], prune: bool = True, share_best: bool = True):
     """One-GPU emulation of N ranks running AT THE SAME TIME: every slab is a
     job of ONE persistent launch, and slab g+1's first strip consumes slab g's
     last strip through the same ext_in / ext_out boundary path (sys-scope
     release / acquire, __threadfence_system) the NVLink peer stores use.  Jobs
     are claimed job-major, so a strip only waits on an item claimed before it
     and the launch stays deadlock-free (separate waiting launches on one GPU
-    are not: B200_PROFILING.md).  Returns the merged (score, i, j) and the
-    per-slab results."""
+    are not: B200_PROFILING.md).  With share_best every slab prunes with the
+    running best of the whole pass (swb_pass_desc.shared_best).  Returns the
+    merged (score, i, j) and the per-slab results."""
     bounds = [Boundary(S.ctx, S.n2) for _ in slabs[1:]]
+    best = Boundary(S.ctx, 1) if share_best else None  # its progress word: the shared best
     old_jm = S.ctx.get_option("job_major")
     S.ctx.set_option("rows_per_lane", SLAB_ROWS_PER_LANE)
     S.ctx.set_option("job_major", 1)
@@ -175,14 +181,15 @@ def run_slabs_concurrent(S, slabs: list[Slab], prune: bool = True):
         for g, slab in enumerate(slabs):
             ext_in = (bounds[g - 1].buf, bounds[g - 1].progress) if g > 0 else None
             ext_out = (bounds[g].buf, bounds[g].progress) if g + 1 < len(slabs) else None
-            specs.append(slab_spec(slab, S.n1, S.n2, ext_in, ext_out, prune))
+            specs.append(slab_spec(slab, S.n1, S.n2, ext_in, ext_out, prune,
+                                   best.progress if best else 0))
         results = S.run(specs)
         merged = merge_best([(r.best_score, r.best_i, r.best_j) for r in results], TRACK_MIN)
         return merged, results
     finally:
         S.ctx.set_option("rows_per_lane", 0)
         S.ctx.set_option("job_major", old_jm)
-        for b in bounds:
+        for b in bounds + ([best] if best else []):
             b.free()
 
 
@@ -238,19 +245,22 @@ def align_distributed(seq1, seq2, scheme, config=None, report: dict | None = Non
         slabs = slab_partition(S.n1, world, SLAB_STRIP_ROWS)
         me = slabs[rank]
         inbound = Boundary(ctx, S.n2) if rank > 0 else None
+        best = Boundary(ctx, 1) if rank == 0 else None  # shared running best (rank 0's memory)
         handles = [None] * world
-        dist.all_gather_object(handles, inbound.export() if inbound else None)
+        dist.all_gather_object(handles, (inbound.export() if inbound else None,
+                                         ipc_export(ctx, best.progress) if best else None))
         ext_out = None
         if rank + 1 < world:
-            hb, hp = handles[rank + 1]
+            hb, hp = handles[rank + 1][0]
             ext_out = (ipc_import(ctx, hb), ipc_import(ctx, hp))
         ext_in = (inbound.buf, inbound.progress) if inbound else None
+        shared_best = best.progress if best else ipc_import(ctx, handles[0][1])
         try:
             dist.barrier()
             if world > 1:
                 ctx.set_option("rows_per_lane", SLAB_ROWS_PER_LANE)
             try:
-                spec = slab_spec(me, S.n1, S.n2, ext_in, ext_out, cfg.prune)
+                spec = slab_spec(me, S.n1, S.n2, ext_in, ext_out, cfg.prune, shared_best)
                 spec["bound_write"] = 1 if S.bounds else 0
                 res = S.run([spec])[0]
             finally:
@@ -285,9 +295,13 @@ def align_distributed(seq1, seq2, scheme, config=None, report: dict | None = Non
             if ext_out:
                 ctx.lib.swb_ipc_close(ctx.ptr, ext_out[0])
                 ctx.lib.swb_ipc_close(ctx.ptr, ext_out[1])
+            if not best:
+                ctx.lib.swb_ipc_close(ctx.ptr, shared_best)
             dist.barrier()
             if inbound:
                 inbound.free()
+            if best:
+                best.free()
     sc, st, en, pst, ops = out[0]
     if sc == 0:
         return AlignmentSummary.empty(), AlignmentPath.empty()

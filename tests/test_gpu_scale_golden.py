@@ -81,17 +81,35 @@ def test_c2_row_slabs(c2, nslabs):
 
 
 @pytest.mark.parametrize("nslabs", [2, 4, 8])
-@pytest.mark.parametrize("prune", [True, False])
-def test_c2_row_slabs_concurrent(c2, nslabs, prune):
+@pytest.mark.parametrize("prune,share", [(True, True), (True, False), (False, False)])
+def test_c2_row_slabs_concurrent(c2, nslabs, prune, share):
     """The N-rank boundary protocol with every rank running at once: all slabs
-    in one launch, each consuming its predecessor through the ext path."""
+    in one launch, each consuming its predecessor through the ext path, with
+    and without the running best shared between slabs."""
     _, _, a, b = c2
     g = GOLDEN["C2"]
+    pruned = []
     for _ in range(3):
         with Session(get_context(0), a, b, SCHEME) as S:
-            merged, res = run_slabs_concurrent(S, slab_partition(S.n1, nslabs, SLAB_STRIP_ROWS), prune)
+            merged, res = run_slabs_concurrent(S, slab_partition(S.n1, nslabs, SLAB_STRIP_ROWS),
+                                               prune, share)
         assert (merged[0], [merged[1] + 1, merged[2] + 1]) == (g["score"], g["end"])
         assert all(r.kernel == "packed16x2" for r in res)
+        pruned.append(sum(r.pruned_blocks for r in res))
+    if not prune:
+        assert max(pruned) == 0
+
+
+def test_shared_best_prunes_more(c2):
+    """Slabs below the alignment's start prune with the whole pass's best when
+    it is shared (swb_pass_desc.shared_best) and far less on their own."""
+    _, _, a, b = c2
+    out = {}
+    for share in (False, True):
+        with Session(get_context(0), a, b, SCHEME) as S:
+            _, res = run_slabs_concurrent(S, slab_partition(S.n1, 8, SLAB_STRIP_ROWS), True, share)
+        out[share] = sum(r.pruned_blocks for r in res)
+    assert out[True] > out[False]
 
 
 def _check_align(name, cfg=None):
