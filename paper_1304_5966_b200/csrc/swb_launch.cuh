@@ -1,0 +1,121 @@
+// Kernel instantiation and launch (shared by the swb_launch_*.cu translation
+// units, which compile the pass kernels in parallel; swb_pass.cu holds the
+// host logic).  Each dispatch function launches (P != null) or reports the
+// occupancy (occ_out != null) of one kernel family for rows-per-lane R.
+#pragma once
+
+#include <algorithm>
+
+#include "swb_kernels.cuh"
+#include "swb_passes.h"
+#include "swb_x2.cuh"
+
+namespace swb {
+
+// Rows-per-lane instantiations.  Local TRACK_MIN passes (phase 1, split) get a
+// dense set so a single large pass can be cut into exactly as many warp-strips
+// as the SM sub-partitions hold; the other modes get a coarse set.
+constexpr int kLocalR[] = {8, 16, 20, 24, 28, 32};
+constexpr int kOtherR[] = {2, 8, 16, 24, 32};
+// Shared-table kernels (large alphabets): few strip heights.
+constexpr int kBigLocalR[] = {8, 16};
+constexpr int kBigOtherR[] = {8};
+// packed 16x2 phase-1 kernel (swb_x2.cuh): R packed rows per lane, 64R rows per item
+constexpr int kX2R[] = {8, 10, 12, 14, 16};
+constexpr int kX2SlabR = 16;  // multigpu.SLAB_ROWS_PER_LANE x 32 rows = 64 x 16
+// final rows (split mode) are instantiated for the two largest heights only
+constexpr int kX2FinalR[] = {14, 16};
+
+int dispatch_local(swb_ctx* ctx, int R, const PassParams* P, long long items, int track,
+                   int ctas_per_sm, int* occ_out);
+int dispatch_other_none(swb_ctx* ctx, int R, const PassParams* P, long long items,
+                        int ctas_per_sm, int* occ_out);
+int dispatch_other_track(swb_ctx* ctx, int R, const PassParams* P, long long items, int track,
+                         int ctas_per_sm, int* occ_out);
+int dispatch_big(swb_ctx* ctx, int R, const PassParams* P, long long items, bool local, int track,
+                 int ctas_per_sm, int* occ_out);
+int dispatch_x2(swb_ctx* ctx, int R, const PassParams* P, long long items, int ctas_per_sm,
+                int* occ_out, bool wild = false, bool final_rows = false);
+
+// checked builds: each translation unit reports (and clears) its own record
+int chk_take_local(long long* out);
+int chk_take_other(long long* out);
+int chk_take_track(long long* out);
+int chk_take_big(long long* out);
+int chk_take_x2(long long* out);
+
+#ifdef SWB_CHECKED
+#define SWB_CHK_TAKE(name)                                                          \
+  int name(long long* out) {                                                        \
+    if (cudaMemcpyFromSymbol(out, g_swb_chk, 4 * sizeof(long long)) != cudaSuccess) \
+      return -1;                                                                    \
+    const long long zero[4] = {0, 0, 0, 0};                                         \
+    cudaMemcpyToSymbol(g_swb_chk, zero, sizeof(zero));                              \
+    return 0;                                                                       \
+  }
+#else
+#define SWB_CHK_TAKE(name)  \
+  int name(long long* out) { \
+    out[0] = 0;             \
+    return 0;               \
+  }
+#endif
+
+template <int R, bool LOCAL, int TRACK, bool BIG = false>
+int kernel_occupancy(int* per_sm) {
+  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      per_sm, pass_kernel<R, LOCAL, TRACK, BIG>, 128, 0);
+}
+
+template <typename K>
+int launch_any(swb_ctx* ctx, K kern, const PassParams& Pin, long long items, int ctas_per_sm) {
+  PassParams P = Pin;
+  int per_sm = 0;
+  SWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, 0));
+  if (per_sm < 1) return swb_fail(SWB_ECUDA, "pass kernel does not fit on an SM");
+  if (ctas_per_sm > 0 && per_sm > ctas_per_sm) per_sm = ctas_per_sm;
+  if (P.chunk > 0) {
+    const long long cap = (long long)per_sm * ctx->sms;
+    const int grid = (int)std::min(cap, std::max((long long)P.total_items, 1LL));
+    kern<<<grid, 128, 0, ctx->stream>>>(P);
+    ctx->launches++;
+    SWB_CUDA(cudaGetLastError());
+    return SWB_OK;
+  }
+  if (ctx->claim_mode != 2 && (ctx->claim_mode == 1 || (P.njobs <= 4 && !P.warp_claim)) &&
+      per_sm <= 2 && items > (long long)ctx->sms * 4) {
+    // one CTA per SM, per_sm warps per sub-partition, adjacent strips paired
+    const int threads = 128 * per_sm;
+    int fit = 0;
+    SWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, kern, threads, 0));
+    if (fit >= 1) {
+      // adjacent strips of one chain share a sub-partition: job-major order
+      P.item_map = nullptr;
+      P.group = 4 * per_sm;
+      P.mirror = (per_sm == 2 && items <= 8LL * ctx->sms && ctx->proto != 8) ? 1 : 0;
+      // dynamic shared memory pins the layout to exactly one CTA per SM
+      const int pin = 120 * 1024;
+      SWB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pin));
+      kern<<<ctx->sms, threads, pin, ctx->stream>>>(P);
+      ctx->launches++;
+      SWB_CUDA(cudaGetLastError());
+      return SWB_OK;
+    }
+  }
+  P.group = 0;
+  P.mirror = 0;
+  long long cap = (long long)per_sm * ctx->sms;
+  long long need = (items + 3) / 4;
+  int grid = (int)std::min(cap, std::max(need, 1LL));
+  kern<<<grid, 128, 0, ctx->stream>>>(P);
+  ctx->launches++;
+  SWB_CUDA(cudaGetLastError());
+  return SWB_OK;
+}
+
+template <int R, bool LOCAL, int TRACK, bool BIG = false>
+int launch_kernel(swb_ctx* ctx, const PassParams& Pin, long long items, int ctas_per_sm) {
+  return launch_any(ctx, pass_kernel<R, LOCAL, TRACK, BIG>, Pin, items, ctas_per_sm);
+}
+
+}  // namespace swb

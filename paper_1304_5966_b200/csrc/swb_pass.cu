@@ -8,9 +8,7 @@
 #include <cstring>
 #include <vector>
 
-#include "swb_kernels.cuh"
-#include "swb_x2.cuh"
-#include "swb_passes.h"
+#include "swb_launch.cuh"
 
 using namespace swb;
 
@@ -103,171 +101,12 @@ int swb_resolve_seq(swb_ctx* ctx, int32_t id, int64_t off, int64_t len, int32_t 
 
 namespace {
 
-// Rows-per-lane instantiations.  Local TRACK_MIN passes (phase 1, split) get a
-// dense set so a single large pass can be cut into exactly as many warp-strips
-// as the SM sub-partitions hold; the other modes get a coarse set.
-constexpr int kLocalR[] = {8, 16, 20, 24, 28, 32};
-constexpr int kOtherR[] = {2, 8, 16, 24, 32};
-
-template <int R, bool LOCAL, int TRACK, bool BIG = false>
-int kernel_occupancy(int* per_sm) {
-  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      per_sm, pass_kernel<R, LOCAL, TRACK, BIG>, 128, 0);
-}
-
-template <typename K>
-int launch_any(swb_ctx* ctx, K kern, const PassParams& Pin, long long items, int ctas_per_sm) {
-  PassParams P = Pin;
-  int per_sm = 0;
-  SWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, 0));
-  if (per_sm < 1) return swb_fail(SWB_ECUDA, "pass kernel does not fit on an SM");
-  if (ctas_per_sm > 0 && per_sm > ctas_per_sm) per_sm = ctas_per_sm;
-  if (P.chunk > 0) {
-    const long long cap = (long long)per_sm * ctx->sms;
-    const int grid = (int)std::min(cap, std::max((long long)P.total_items, 1LL));
-    kern<<<grid, 128, 0, ctx->stream>>>(P);
-    ctx->launches++;
-    SWB_CUDA(cudaGetLastError());
-    return SWB_OK;
-  }
-  if (ctx->claim_mode != 2 && (ctx->claim_mode == 1 || (P.njobs <= 4 && !P.warp_claim)) &&
-      per_sm <= 2 && items > (long long)ctx->sms * 4) {
-    // one CTA per SM, per_sm warps per sub-partition, adjacent strips paired
-    const int threads = 128 * per_sm;
-    int fit = 0;
-    SWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, kern, threads, 0));
-    if (fit >= 1) {
-      // adjacent strips of one chain share a sub-partition: job-major order
-      P.item_map = nullptr;
-      P.group = 4 * per_sm;
-      P.mirror = (per_sm == 2 && items <= 8LL * ctx->sms && ctx->proto != 8) ? 1 : 0;
-      // dynamic shared memory pins the layout to exactly one CTA per SM
-      const int pin = 120 * 1024;
-      SWB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pin));
-      kern<<<ctx->sms, threads, pin, ctx->stream>>>(P);
-      ctx->launches++;
-      SWB_CUDA(cudaGetLastError());
-      return SWB_OK;
-    }
-  }
-  P.group = 0;
-  P.mirror = 0;
-  long long cap = (long long)per_sm * ctx->sms;
-  long long need = (items + 3) / 4;
-  int grid = (int)std::min(cap, std::max(need, 1LL));
-  kern<<<grid, 128, 0, ctx->stream>>>(P);
-  ctx->launches++;
-  SWB_CUDA(cudaGetLastError());
-  return SWB_OK;
-}
-
-template <int R, bool LOCAL, int TRACK, bool BIG = false>
-int launch_kernel(swb_ctx* ctx, const PassParams& Pin, long long items, int ctas_per_sm) {
-  return launch_any(ctx, pass_kernel<R, LOCAL, TRACK, BIG>, Pin, items, ctas_per_sm);
-}
-
-// Shared-table kernels (large alphabets): few strip heights.
-constexpr int kBigLocalR[] = {8, 16};
-constexpr int kBigOtherR[] = {8};
-
-template <int R>
-int dispatch_big_R(swb_ctx* ctx, const PassParams* P, long long items, bool local, int track,
-                   int ctas_per_sm, int* occ_out) {
-  if (local) {
-    if (track != kTrackMin) return swb_fail(SWB_EUNSUPPORTED, "local passes support TRACK_MIN only");
-    if (occ_out) return kernel_occupancy<R, true, kTrackMin, true>(occ_out);
-    return launch_kernel<R, true, kTrackMin, true>(ctx, *P, items, ctas_per_sm);
-  }
-  if (track == kTrackNone) {
-    if (occ_out) return kernel_occupancy<R, false, kTrackNone, true>(occ_out);
-    return launch_kernel<R, false, kTrackNone, true>(ctx, *P, items, ctas_per_sm);
-  }
-  if (track == kTrackMin) {
-    if (occ_out) return kernel_occupancy<R, false, kTrackMin, true>(occ_out);
-    return launch_kernel<R, false, kTrackMin, true>(ctx, *P, items, ctas_per_sm);
-  }
-  if (occ_out) return kernel_occupancy<R, false, kTrackMax, true>(occ_out);
-  return launch_kernel<R, false, kTrackMax, true>(ctx, *P, items, ctas_per_sm);
-}
-
-int dispatch_big(swb_ctx* ctx, int R, const PassParams* P, long long items, bool local, int track,
-                 int ctas_per_sm, int* occ_out) {
-  if (R == 8) return dispatch_big_R<8>(ctx, P, items, local, track, ctas_per_sm, occ_out);
-  if (R == 16 && local) return dispatch_big_R<16>(ctx, P, items, local, track, ctas_per_sm, occ_out);
-  return swb_fail(SWB_EINVAL, "rows_per_lane %d not instantiated for large alphabets", R);
-}
-
-// packed 16x2 phase-1 kernel (swb_x2.cuh): R packed rows per lane, 64R rows per item
-constexpr int kX2R[] = {8, 10, 12, 14, 16};
-constexpr int kX2SlabR = 16;  // multigpu.SLAB_ROWS_PER_LANE x 32 rows = 64 x 16
-
-template <int R>
-int dispatch_x2_R(swb_ctx* ctx, const PassParams* P, long long items, int ctas_per_sm,
-                  int* occ_out, bool wild) {
-  if (occ_out)
-    return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ_out, pass_kernel_x2<R, false>,
-                                                              128, 0);
-  return wild ? launch_any(ctx, pass_kernel_x2<R, true>, *P, items, ctas_per_sm)
-              : launch_any(ctx, pass_kernel_x2<R, false>, *P, items, ctas_per_sm);
-}
-
-int dispatch_x2(swb_ctx* ctx, int R, const PassParams* P, long long items, int ctas_per_sm,
-                int* occ_out, bool wild = false) {
-  switch (R) {
-    case 8: return dispatch_x2_R<8>(ctx, P, items, ctas_per_sm, occ_out, wild);
-    case 10: return dispatch_x2_R<10>(ctx, P, items, ctas_per_sm, occ_out, wild);
-    case 12: return dispatch_x2_R<12>(ctx, P, items, ctas_per_sm, occ_out, wild);
-    case 14: return dispatch_x2_R<14>(ctx, P, items, ctas_per_sm, occ_out, wild);
-    case 16: return dispatch_x2_R<16>(ctx, P, items, ctas_per_sm, occ_out, wild);
-    default: break;
-  }
-  return swb_fail(SWB_EINVAL, "packed rows_per_lane %d not instantiated", R);
-}
-
-template <int R>
-int dispatch_R(swb_ctx* ctx, const PassParams* P, long long items, bool local, int track,
-               int ctas_per_sm, int* occ_out) {
-  if (local) {
-    if (track != kTrackMin) return swb_fail(SWB_EUNSUPPORTED, "local passes support TRACK_MIN only");
-    if (occ_out) return kernel_occupancy<R, true, kTrackMin>(occ_out);
-    return launch_kernel<R, true, kTrackMin>(ctx, *P, items, ctas_per_sm);
-  }
-  if (track == kTrackNone) {
-    if (occ_out) return kernel_occupancy<R, false, kTrackNone>(occ_out);
-    return launch_kernel<R, false, kTrackNone>(ctx, *P, items, ctas_per_sm);
-  }
-  if (track == kTrackMin) {
-    if (occ_out) return kernel_occupancy<R, false, kTrackMin>(occ_out);
-    return launch_kernel<R, false, kTrackMin>(ctx, *P, items, ctas_per_sm);
-  }
-  if (occ_out) return kernel_occupancy<R, false, kTrackMax>(occ_out);
-  return launch_kernel<R, false, kTrackMax>(ctx, *P, items, ctas_per_sm);
-}
-
-// Launch (P != null) or query occupancy (occ_out != null) for rows-per-lane R.
+// Lane-kernel dispatch (swb_launch_local.cu / _none.cu / _track.cu).
 int dispatch(swb_ctx* ctx, int R, const PassParams* P, long long items, bool local, int track,
              int ctas_per_sm, int* occ_out) {
-  if (local) {
-    switch (R) {
-      case 8: return dispatch_R<8>(ctx, P, items, local, track, ctas_per_sm, occ_out);
-      case 16: return dispatch_R<16>(ctx, P, items, local, track, ctas_per_sm, occ_out);
-      case 20: return dispatch_R<20>(ctx, P, items, local, track, ctas_per_sm, occ_out);
-      case 24: return dispatch_R<24>(ctx, P, items, local, track, ctas_per_sm, occ_out);
-      case 28: return dispatch_R<28>(ctx, P, items, local, track, ctas_per_sm, occ_out);
-      case 32: return dispatch_R<32>(ctx, P, items, local, track, ctas_per_sm, occ_out);
-      default: break;
-    }
-  } else {
-    switch (R) {
-      case 2: return dispatch_R<2>(ctx, P, items, local, track, ctas_per_sm, occ_out);
-      case 8: return dispatch_R<8>(ctx, P, items, local, track, ctas_per_sm, occ_out);
-      case 16: return dispatch_R<16>(ctx, P, items, local, track, ctas_per_sm, occ_out);
-      case 24: return dispatch_R<24>(ctx, P, items, local, track, ctas_per_sm, occ_out);
-      case 32: return dispatch_R<32>(ctx, P, items, local, track, ctas_per_sm, occ_out);
-      default: break;
-    }
-  }
-  return swb_fail(SWB_EINVAL, "rows_per_lane %d not instantiated for this pass mode", R);
+  if (local) return dispatch_local(ctx, R, P, items, track, ctas_per_sm, occ_out);
+  if (track == kTrackNone) return dispatch_other_none(ctx, R, P, items, ctas_per_sm, occ_out);
+  return dispatch_other_track(ctx, R, P, items, track, ctas_per_sm, occ_out);
 }
 
 // Launch-shape model.  A warp-step costs ~5.7 integer-ALU
@@ -281,8 +120,11 @@ struct Shape {
 
 Shape choose_shape(swb_ctx* ctx, const std::vector<PassReq*>& jobs, bool local, int track,
                    bool x2, bool big) {
-  const int* cand = x2 ? kX2R : big ? (local ? kBigLocalR : kBigOtherR) : (local ? kLocalR : kOtherR);
-  const int ncand = x2    ? (int)(sizeof(kX2R) / sizeof(int))
+  bool x2f = false;  // packed kernel with final rows: its own instantiations
+  for (const PassReq* r : jobs) x2f |= x2 && r->want_final;
+  const int* cand = x2f ? kX2FinalR : x2 ? kX2R : big ? (local ? kBigLocalR : kBigOtherR) : (local ? kLocalR : kOtherR);
+  const int ncand = x2f   ? (int)(sizeof(kX2FinalR) / sizeof(int))
+                    : x2  ? (int)(sizeof(kX2R) / sizeof(int))
                     : big ? (local ? (int)(sizeof(kBigLocalR) / sizeof(int))
                                    : (int)(sizeof(kBigOtherR) / sizeof(int)))
                           : (local ? (int)(sizeof(kLocalR) / sizeof(int))
@@ -294,7 +136,7 @@ Shape choose_shape(swb_ctx* ctx, const std::vector<PassReq*>& jobs, bool local, 
   for (int q = 0; q < ncand; ++q) {
     const int R = cand[q];
     int occ = 0;
-    const int rc = x2    ? dispatch_x2(ctx, R, nullptr, 0, 0, &occ)
+    const int rc = x2    ? dispatch_x2(ctx, R, nullptr, 0, 0, &occ, false, x2f)
                    : big ? dispatch_big(ctx, R, nullptr, 0, local, track, 0, &occ)
                          : dispatch(ctx, R, nullptr, 0, local, track, 0, &occ);
     if (rc != cudaSuccess || occ < 1) continue;
@@ -414,7 +256,7 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
       if (v < 0 || v > 127) x2_scheme = false;
     }
   for (PassReq& r : reqs)
-    r.x2 = x2_scheme && r.local && r.track == kTrackMin && !r.has_band && !r.want_final &&
+    r.x2 = x2_scheme && r.local && r.track == kTrackMin && !r.has_band &&
            r.prune <= 1 &&
            // rows_per_lane forces the 32-bit kernel, except on row slabs where
            // it only fixes the strip granularity (64 x kX2SlabR rows here)
@@ -689,7 +531,9 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     int rc;
     int ctas = ctx->max_ctas_per_sm ? ctx->max_ctas_per_sm : cls_ctas[order[g0]];
     P.wild_const = wild_const;
-    rc = head.x2  ? dispatch_x2(ctx, R, &P, item, ctas, nullptr, head.x2_wild)
+    bool any_final_x2 = false;
+    for (size_t t = g0; t < g1; ++t) any_final_x2 |= head.x2 && reqs[order[t]].want_final;
+    rc = head.x2  ? dispatch_x2(ctx, R, &P, item, ctas, nullptr, head.x2_wild, any_final_x2)
          : sc.big ? dispatch_big(ctx, R, &P, item, head.local, head.track, ctas, nullptr)
                   : dispatch(ctx, R, &P, item, head.local, head.track, ctas, nullptr);
     if (rc) return rc;
@@ -734,13 +578,13 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
 #ifdef SWB_CHECKED
     {
       long long chk[4];
-      SWB_CUDA(cudaMemcpyFromSymbol(chk, g_swb_chk, sizeof(chk)));
-      if (chk[0]) {
-        const long long zero[4] = {0, 0, 0, 0};
-        SWB_CUDA(cudaMemcpyToSymbol(g_swb_chk, zero, sizeof(zero)));
-        return swb_fail(SWB_ECUDA,
-                        "device bounds check: %lld bad indices, first at swb_kernels.cuh:%lld "
-                        "(index %lld outside [0, %lld))", chk[0], chk[1], chk[2], chk[3]);
+      int (*takes[])(long long*) = {chk_take_local, chk_take_other, chk_take_track, chk_take_big,
+                                    chk_take_x2};
+      for (auto take : takes) {
+        if (take(chk) == 0 && chk[0])
+          return swb_fail(SWB_ECUDA,
+                          "device bounds check: %lld bad indices, first at swb_kernels.cuh:%lld "
+                          "(index %lld outside [0, %lld))", chk[0], chk[1], chk[2], chk[3]);
       }
     }
 #endif

@@ -84,7 +84,7 @@ __device__ __forceinline__ int clamp_rel(long long v) {
   return v < 0 ? 0 : (v > 32767 ? 32767 : (int)v);
 }
 
-template <int R, bool WILD>
+template <int R, bool WILD, bool FINAL>
 __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& Jg, int s,
                                           WarpSmemX2* sm, const uint32_t* __restrict__ tw_s) {
   static_assert(R <= 32, "rank field is 5 bits");
@@ -190,6 +190,18 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     tile_range(J.map_r0, J.map_rdir, R0, r_hi, J.map_nr, bw.rt_lo, bw.rt_hi);
   }
 
+  // FINAL (last item of a pass that wants its final rows, split mode): the lane,
+  // packed row and half holding DP row n1 write (H, F) of every column they
+  // compute; skipped cells keep the fill values written before the launch
+  int lstar = -1, rstar = 0, hstar = 0;
+  if (FINAL) {
+    const int off = n1 - 1 - R0;
+    hstar = off >= 32 * R ? 1 : 0;
+    const int o2 = off - hstar * 32 * R;
+    lstar = o2 / R;
+    rstar = o2 % R;
+  }
+
   int known_prog = 0, prune_seen = 0, published = 0;
   int code_next = (lane < n2) ? (int)J.cols[(long long)lane * J.cstep] : 0;
   long long pruned_blocks = 0, exec_blocks = 0, wait_cycles = 0;
@@ -224,6 +236,7 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     uint32_t hab = up_h;
     uint32_t cm = guard ? 0u : bk2, kp = 0u;
     uint32_t vmx = 0u, vkp = 0u;
+    uint32_t fh = 0u, ff = 0u;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const uint32_t sv = prmt(tl, th, sel[r]);
@@ -237,6 +250,10 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
       d = Hin[r];
       Hout[r] = guard ? ((hm & ~keep) | (Hin[r] & keep)) : hm;
       hab = h2m;
+      if (FINAL && r == rstar) {
+        fh = hm;
+        ff = fv;
+      }
       if (MODE == 2) {
         if (r & 1) vmx = vimax3_2(vmx, vkp, hm);
         else if (r == R - 1) vmx = vimax3_2(vmx, hm, hm);
@@ -258,6 +275,14 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
       sm->trk[k][lane] = bk2;
     }
     if (lane == 31 && actB) sm->out[k] = make_uint2(out_hm, out_f);
+    if (FINAL && lane == lstar) {
+      const int col = hstar ? colB : colA;
+      if (col >= 0 && col < n2) {
+        const int off = base - kX2Off;
+        J.fin_h[col] = (hstar ? hi16(fh) : lo16(fh)) + off + goe;
+        J.fin_f[col] = (hstar ? hi16(ff) : lo16(ff)) + off;
+      }
+    }
   };
 
   for (int s0 = 0; s0 < s_end; s0 += 32) {
@@ -566,7 +591,9 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
   }
 }
 
-template <int R, bool WILD>
+// FINAL kernels also serve passes that want their final rows (split mode): the
+// last item of such a pass runs the FINAL strip code.
+template <int R, bool WILD, bool FINAL>
 __global__ void __launch_bounds__(256, 1) pass_kernel_x2(const PassParams P) {
   __shared__ WarpSmemX2 wsm[8];
   __shared__ uint32_t tw_s[8];
@@ -579,7 +606,10 @@ __global__ void __launch_bounds__(256, 1) pass_kernel_x2(const PassParams P) {
   auto run = [&](long long item) {
     int s = 0;
     const int j = item_job(P, item, &s);
-    run_strip_x2<R, WILD>(P, P.jobs[j], s, sm, tw_s);
+    if (FINAL && P.jobs[j].want_final && s == P.jobs[j].nstrips - 1)
+      run_strip_x2<R, WILD, FINAL>(P, P.jobs[j], s, sm, tw_s);
+    else
+      run_strip_x2<R, WILD, false>(P, P.jobs[j], s, sm, tw_s);
   };
   if (P.group > 0) {
     const int w = (int)(blockDim.x >> 7);

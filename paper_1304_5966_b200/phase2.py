@@ -66,9 +66,15 @@ def oriented_interval(band: BandSpec, score: int, rows: int, cols: int,
 
 def restricted_search(S: Session, rows: tuple, cols: tuple, target: int, interval,
                       preopen_vgap: bool = False, track: int = TRACK_MAX,
-                      gap_tolerant: bool = False, bounds: bool = False) -> tuple[int, int]:
+                      gap_tolerant: bool = False, bounds: bool = False,
+                      maps: tuple[int, int] = (1, 2)) -> tuple[int, int]:
     """Origin-anchored pass returning the cell that attains `target`
-    (phase2.py:82-138).  rows/cols are (offset, length, reversed) slices."""
+    (phase2.py:82-138).  rows/cols are (offset, length, reversed) slices.
+    With bounds, the pass skips blocks the tile map maps[0] proves useless and
+    records its own bounds in map maps[1] (1 forward, 2 reverse; DESIGN.md
+    §3.6): a reversed search (phase 2) reads the forward map of the local pass
+    and writes the reverse map, a forward search from a known start (split
+    mode) reads the reverse map and writes the forward one."""
     if gap_tolerant or preopen_vgap:
         border = "continue" if preopen_vgap else "free"
     else:
@@ -79,7 +85,7 @@ def restricted_search(S: Session, rows: tuple, cols: tuple, target: int, interva
     # start) can add, and this pass records its own tile map for phase 3 (§3.6).
     extra = {}
     if bounds and S.bounds and S.target_prune:
-        extra = dict(bound_read=1, bound_write=2, bound_offset=bound_slack(S.scheme))
+        extra = dict(bound_read=maps[0], bound_write=maps[1], bound_offset=bound_slack(S.scheme))
     res = S.run([dict(rows=rows, cols=cols, border=border, clamp=False, track=track,
                       band=interval, prune=2 if S.target_prune else 0,
                       prune_target=target, **extra)])[0]

@@ -225,6 +225,18 @@ def solve_rect(S: Session, sub: Subproblem, leaf_limit: int = DEFAULT_LEAF_LIMIT
     return ops
 
 
+def solve_rects(S: Session, subs: list[Subproblem], leaf_limit: int = DEFAULT_LEAF_LIMIT,
+                band: bool = True, stats: dict | None = None) -> np.ndarray:
+    """solve_rect for consecutive rectangles of one path (split mode's two
+    halves of a midpoint alignment): one breadth-first recursion over all of
+    them, so every level's crossings of every rectangle share a launch.  The
+    leaves stay in path order, so the result is the concatenation of the
+    rectangles' op sequences."""
+    leaves = collect_leaves(S, _as_array(subs, getattr(S, "bounds", False)), leaf_limit, band,
+                            stats)
+    return solve_leaves(S, leaves, band)
+
+
 def reconstruct(S: Session, summary: AlignmentSummary, leaf_limit: int = DEFAULT_LEAF_LIMIT,
                 band: bool = True, stats: dict | None = None) -> AlignmentPath:
     """Full path for a summary from phases 1 and 2 (phase3.py:289-312)."""

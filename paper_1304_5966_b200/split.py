@@ -2,10 +2,24 @@
 
 The upper-forward and lower-reversed local passes run as two jobs of ONE
 persistent device launch (on one B200 the "two cards" of the paper are two
-independent job chains sharing the SMs).  Their final rows meet at the middle
-row exactly like a Myers-Miller split; the three candidate optima are
-classified with the reference's tie order and each case is finished with the
+job chains sharing the SMs; across GPUs, multigpu.split_align_distributed
+gives each half its own GPU group).  Their final rows meet at the middle row
+exactly like a Myers-Miller split; the three candidate optima are classified
+with the reference's tie order and each case is finished with the
 phase-2/phase-3 device operators.
+
+Fast path: both halves run on the packed 16x2 kernel with
+phase-1 pruning against a running best SHARED by the two halves, each half's
+bound counting the rows of the other half (rows_after), so every cell of an
+optimal alignment — upper, lower or through the middle row — keeps its exact
+value, while cells that cannot reach the optimum become fill.  The combine is
+exact wherever it matters: a column whose true sum hh or ff equals the
+optimum lies on an optimal path; any other column can only be
+under-estimated, which cannot change the classification (ties included).  The
+halves also record tile bound maps (upper: forward map, lower: reverse map of
+the reversed local pass = a bound on the best path leaving a cell), so the
+finishing restricted searches and Myers-Miller passes skip tiles as in
+split=1.
 """
 from __future__ import annotations
 
@@ -60,19 +74,55 @@ def _search_interval(score, rows, cols, scheme, band):
 
 
 def split_align(S: Session, leaf_limit: int = phase3.DEFAULT_LEAF_LIMIT, band: bool = True,
-                report: dict | None = None) -> tuple[AlignmentSummary, AlignmentPath]:
-    """split.split_align (split.py:84-182)."""
+                report: dict | None = None, fast: bool = True
+                ) -> tuple[AlignmentSummary, AlignmentPath]:
+    """split.split_align (split.py:84-182).  fast=False runs the two halves as
+    the reference does (no pruning, no tile maps)."""
+    import time
+    from .multigpu import Boundary
+    t0 = time.perf_counter()
     n1, n2 = S.n1, S.n2
     mid = n1 // 2
-    go = S.scheme.gap_open
-    specs = [dict(rows=(mid, n1 - mid, 1), cols=(0, n2, 1), border="local", clamp=True,
-                  track=TRACK_MIN, want_final=True)]
-    if mid >= 1:
-        specs.insert(0, dict(rows=(0, mid, 0), cols=(0, n2, 0), border="local", clamp=True,
-                             track=TRACK_MIN, want_final=True))
-    res = S.run(specs)
+    best = None
+    if fast:
+        S.reset_bounds()
+        best = Boundary(S.ctx, 1)  # its progress word: the running best of both halves
+    try:
+        specs = half_specs(n1, n2, mid, best.progress if best else 0)
+        res = S.run(specs if mid >= 1 else specs[1:])
+    finally:
+        if best is not None:
+            best.free()
     res_up, res_dn = (res[0], res[1]) if mid >= 1 else (None, res[0])
+    t1 = time.perf_counter()
+    out = combine_and_finish(S, res_up, res_dn, mid, leaf_limit, band, report)
+    if report is not None:
+        report.update(phase_seconds=(t1 - t0, time.perf_counter() - t1),
+                      halves_cells=(res_up.cells_executed if res_up else 0) + res_dn.cells_executed)
+    return out
 
+
+def half_specs(n1: int, n2: int, mid: int, shared_best: int) -> list[dict]:
+    """Session.run() specs of the upper-forward and lower-reversed local passes
+    (split.py:64-81, :103-122).  With a shared best (fast path) both prune
+    against the running best of the two, each counting the other half's rows
+    (rows_after), and they record the forward / reverse tile maps."""
+    up = dict(rows=(0, mid, 0), cols=(0, n2, 0), border="local", clamp=True, track=TRACK_MIN,
+              want_final=True)
+    dn = dict(rows=(mid, n1 - mid, 1), cols=(0, n2, 1), border="local", clamp=True,
+              track=TRACK_MIN, want_final=True)
+    if shared_best:
+        up.update(prune=True, shared_best=shared_best, rows_after=n1 - mid, bound_write=1)
+        dn.update(prune=True, shared_best=shared_best, rows_after=mid, bound_write=2)
+    return [up, dn]
+
+
+def combine_and_finish(S: Session, res_up, res_dn, mid: int, leaf_limit: int, band: bool,
+                       report: dict | None) -> tuple[AlignmentSummary, AlignmentPath]:
+    """Middle-row combine of the two halves' results (split.py:124-149) and the
+    three-case finish (split.py:150-182); shared with the multi-GPU split."""
+    n1, n2 = S.n1, S.n2
+    go = S.scheme.gap_open
     if res_up is not None:
         upper_score = max(0, res_up.best_score)
         upper_end = Coord(res_up.best_i + 1, res_up.best_j + 1) if upper_score > 0 else Coord(0, 0)
@@ -121,7 +171,7 @@ def _finish_lower(S, mc, leaf_limit, band):
     rows, cols = S.n1 - start.i, S.n2 - start.j
     iv = _search_interval(score, rows, cols, S.scheme, band)
     ci, cj = phase2.restricted_search(S, (start.i, rows, 0), (start.j, cols, 0), score, iv,
-                                      track=TRACK_MIN)
+                                      track=TRACK_MIN, bounds=True, maps=(2, 1))
     summary = AlignmentSummary(score, start, Coord(start.i + ci + 1, start.j + cj + 1))
     return summary, phase3.reconstruct(S, summary, leaf_limit, band)
 
@@ -132,27 +182,30 @@ def _finish_midpoint(S, mc, mid, leaf_limit, band):
     cross = Coord(mid, jc)
     upper_target = mc.upper_seg + (go if gap else 0)
     lower_expected = mc.lower_seg + (go if gap else 0)
+    parts = []
     if not gap and mc.upper_seg == 0:
-        ustart, ops_up = cross, np.empty(0, dtype=np.uint8)
+        ustart = cross
     else:
         iv = _search_interval(upper_target, mid, jc, S.scheme, band) if upper_target >= 1 else None
         ri, rj = phase2.restricted_search(S, (0, mid, 1), (0, jc, 1), upper_target, iv,
-                                          preopen_vgap=gap, track=TRACK_MAX, gap_tolerant=True)
+                                          preopen_vgap=gap, track=TRACK_MAX, gap_tolerant=True,
+                                          bounds=True, maps=(1, 2))
         ustart = Coord(mid - ri - 1, jc - rj - 1)
-        ops_up = phase3.solve_rect(
-            S, phase3.Subproblem(ustart, cross, mc.upper_seg, start_vgap=False, end_vgap=gap),
-            leaf_limit, band)
+        parts.append(phase3.Subproblem(ustart, cross, mc.upper_seg, start_vgap=False,
+                                       end_vgap=gap))
     rows, cols = S.n1 - mid, S.n2 - jc
     iv = (_search_interval(lower_expected, rows, cols, S.scheme, band)
           if lower_expected >= 1 else None)
     ci, cj = phase2.restricted_search(S, (mid, rows, 0), (jc, cols, 0), lower_expected, iv,
-                                      preopen_vgap=gap, track=TRACK_MIN, gap_tolerant=True)
+                                      preopen_vgap=gap, track=TRACK_MIN, gap_tolerant=True,
+                                      bounds=True, maps=(2, 1))
     lend = Coord(mid + ci + 1, jc + cj + 1)
-    ops_dn = phase3.solve_rect(
-        S, phase3.Subproblem(cross, lend, lower_expected, start_vgap=gap, end_vgap=False),
-        leaf_limit, band)
-    path = phase3.join_paths([AlignmentPath(ustart, ops_up), AlignmentPath(cross, ops_dn)])
+    parts.append(phase3.Subproblem(cross, lend, lower_expected, start_vgap=gap, end_vgap=False))
+    # both rectangles in one breadth-first recursion (= join_paths of the two)
+    path = AlignmentPath(ustart, phase3.solve_rects(S, parts, leaf_limit, band))
     summary = AlignmentSummary(mc.mid_score, ustart, lend)
+    if path.end != lend:
+        raise ScoreMismatch(f"joined midpoint path ends at {path.end}, expected {lend}")
     achieved = score_of_path(path, phase3._Seq(S.codes1), phase3._Seq(S.codes2), S.scheme)
     if achieved != summary.score:
         raise ScoreMismatch(f"joined midpoint path scores {achieved}, expected {summary.score}")
