@@ -279,7 +279,11 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
       for (PassReq* r : js)
         if (r->ext_out) sh.R = kX2SlabR;  // slabs are cut in multiples of 64 x kX2SlabR rows
     for (PassReq* r : js) {
-      r->R = (r->force_R && !r->x2) ? r->force_R : sh.R;
+      int fr = r->force_R;
+      // shared-table kernels have fewer heights: a forced height (row slabs
+      // use 32) maps to the largest instantiated one, which divides it
+      if (fr && sc.big && (fr > 16 || (!r->local && fr > 8))) fr = r->local ? 16 : 8;
+      r->R = (fr && !r->x2) ? fr : sh.R;
       cls_ctas[r - &reqs[0]] = sh.ctas_per_sm;
     }
     a = b;

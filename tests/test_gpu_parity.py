@@ -42,6 +42,20 @@ def test_golden_medium_and_config1(golden_medium):
         _check_rec(rec)
 
 
+@pytest.mark.parametrize("world", [2, 4])
+def test_golden_split_gpu_groups(golden_medium, golden_protein, world):
+    """align_split goldens through the Figure-1 split across GPU groups
+    (multigpu.run_split_slabs_concurrent: the multi-GPU schedule emulated in
+    one launch; medium inputs leave every group one slab)."""
+    from paper_1304_5966_b200.engine import Session, get_context
+    from paper_1304_5966_b200.multigpu import run_split_slabs_concurrent
+    for rec in golden_medium + golden_protein[::8]:
+        s1, s2, scheme = golden_inputs(rec)
+        with Session(get_context(0), s1.codes, s2.codes, scheme) as S:
+            got = _summ(*run_split_slabs_concurrent(S, world))
+        assert got == rec["align_split"], (rec.get("tag"), got, rec["align_split"])
+
+
 def test_score_only_prune_report(golden_medium):
     rec = [r for r in golden_medium if r["tag"] == "config1"][0]
     s1, s2, scheme = golden_inputs(rec)

@@ -27,7 +27,8 @@ import paper_1304_5966_b200 as swb
 from paper_1304_5966_b200 import AlignConfig, Sequence
 from paper_1304_5966_b200.engine import Session, get_context
 from paper_1304_5966_b200.multigpu import (SLAB_STRIP_ROWS, run_slabs_concurrent,
-                                          run_slabs_sequential, slab_partition)
+                                          run_slabs_sequential, run_split_slabs_concurrent,
+                                          slab_partition)
 
 pytestmark = pytest.mark.gpu
 
@@ -131,6 +132,19 @@ def test_window_align(name):
 
 def test_c3_window_split2():
     _check_align("C3w_split", AlignConfig(split=2))
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_c3_window_split2_gpu_groups(world):
+    """The Figure-1 split across `world` GPUs (upper half on ranks [0, G/2),
+    lower half on [G/2, G), row slabs within each group, one shared running
+    best), emulated in one launch: byte-equal to the reference's split=2."""
+    s1, s2, a, b = pair("C3w_split")
+    g = GOLDEN["C3w_split"]
+    with Session(get_context(0), a, b, SCHEME) as S:
+        summ, path = run_split_slabs_concurrent(S, world)
+    assert (summ.score, list(summ.start), list(summ.end)) == (g["score"], g["start"], g["end"])
+    assert swb.path_to_cigar(path) == g["cigar"]
 
 
 def test_c4_window_score():

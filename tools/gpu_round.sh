@@ -1,4 +1,2 @@
 export SWB_WATCHDOG_MS=120000
-timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/t5.log 2>&1; echo rc=$? >> gpurun_out/t5.log
-timeout 600 python tools/split_probe.py 1000000 5000000 > gpurun_out/sp5_probe.log 2>&1; echo rc=$? >> gpurun_out/sp5_probe.log
-timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu --no-align > gpurun_out/b5.log 2>&1; echo rc=$? >> gpurun_out/b5.log
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_scale_golden.py -q -x -k "groups or split" > gpurun_out/f1s.log 2>&1; echo rc=$? >> gpurun_out/f1s.log
