@@ -58,10 +58,10 @@ ALG_OPS_PER_CELL = 8
 # ALU-pipe instructions the kernels issue per cell:
 #   lane32     PRMT + 4 VIADDMNMX + running max                       = 6
 #   packed16x2 PRMT + VIMNMX3 + 3 VIADDMNMX per two cells (S16x2)   = 2.5
-OPS_PER_CELL = {"lane32": 6.0, "packed16x2": 2.5}
+OPS_PER_CELL = {"lane32": 6.0, "packed16x2": 2.5, "wide64": 6.0}
 # 16-bit ops per lane-op: the packed kernel computes two cells per instruction
-LANES_PER_OP = {"lane32": 1, "packed16x2": 2}
-DTYPE = {"lane32": "int32", "packed16x2": "int16x2"}
+LANES_PER_OP = {"lane32": 1, "packed16x2": 2, "wide64": 1}
+DTYPE = {"lane32": "int32", "packed16x2": "int16x2", "wide64": "int64"}
 GOLDEN_SCALE = ROOT / "tests" / "golden" / "golden_scale.json.gz"
 
 

@@ -155,7 +155,7 @@ typedef struct {
   int64_t tiles_pruned;
   int64_t tiles_banded_out;
   double kernel_ms; /* CUDA-event time of the launch that carried this pass */
-  int32_t kernel;        /* 0: 32-bit lane kernel, 1: packed 16x2 kernel */
+  int32_t kernel;        /* 0: 32-bit lane kernel, 1: packed 16x2 kernel, 2: int64 kernel */
   int32_t rows_per_lane; /* R of that launch (packed: R row pairs per lane) */
 } swb_pass_out;
 

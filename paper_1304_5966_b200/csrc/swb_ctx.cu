@@ -122,7 +122,7 @@ void swb_ctx_destroy(swb_ctx* ctx) {
   }
   swb_buf* bufs[] = {&ctx->jobs,  &ctx->rowbuf, &ctx->progress, &ctx->results, &ctx->finals,
                      &ctx->misc,  &ctx->flush,  &ctx->bmap_fwd, &ctx->bmap_rev, &ctx->bmap_live,
-                     &ctx->pass_finals, &ctx->dbg_buf, &ctx->claim_log};
+                     &ctx->pass_finals, &ctx->dbg_buf, &ctx->claim_log, &ctx->wide_buf};
   if (ctx->tev0) {
     cudaEventDestroy(ctx->tev0);
     cudaEventDestroy(ctx->tev1);

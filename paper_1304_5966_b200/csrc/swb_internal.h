@@ -58,6 +58,7 @@ struct swb_ctx {
   int bmaps_on = 1;             // option "bound_maps": 0 disables reads and writes
   int live_ranges = 3;  // restricted passes: bit 0 late start, bit 1 early exit
   int claim_log_on = 0; // option claim_log: record claims in a device ring (swb_debug_claims)
+  int wide_log2 = 28;   // passes with dynamic range >= 2^wide_log2 run on the int64 kernel
   int watchdog_ms = 0;  // > 0: report a pass launch still running after this long
   int live_big = 3;     // live_ranges bits kept for shared-table (large alphabet) passes
   int p2_R = 8;         // rows per lane of bound-pruned restricted passes (phase 2)
@@ -68,7 +69,7 @@ struct swb_ctx {
   int chain_cta = 1;    // chain-shaped passes in chunks of 4 strips per CTA (shared-memory handoff)   // acquire polling with short back-off in chain-shaped passes
   swb_buf bmap_fwd, bmap_rev, bmap_live;
   // scratch
-  swb_buf dbg_buf, claim_log;      // per-strip diagnostics of the last launch
+  swb_buf dbg_buf, claim_log, wide_buf;      // per-strip diagnostics of the last launch
   swb_buf pass_finals;  // final rows of swb_pass calls (whole call, all launch groups)
   swb_buf jobs, rowbuf, progress, results, finals, misc, host_pinned, flush;
   cudaEvent_t tev0 = nullptr, tev1 = nullptr;

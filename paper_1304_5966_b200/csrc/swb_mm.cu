@@ -47,6 +47,8 @@ __host__ __device__ inline long long left_f64(int border, long long I, int go, i
 
 struct CombineDev {
   const int32_t *uh, *uf, *dh, *df;  // final rows (cell columns 0..cols-1 -> DP 1..cols)
+  // int64 final rows of passes that ran on the wide kernel (swb_wide.cu), else null
+  const long long *uh64, *uf64, *dh64, *df64;
   int32_t cols;
   int32_t rows_up, rows_dn;
   int32_t border_up, border_dn;
@@ -62,16 +64,20 @@ struct CombineOut {
 };
 
 __device__ inline long long up_h(const CombineDev& c, int j, int go, int ge) {
-  return j == 0 ? left_h64(c.border_up, c.rows_up, go, ge) : widen64(c.uh[j - 1]);
+  return j == 0 ? left_h64(c.border_up, c.rows_up, go, ge)
+                : (c.uh64 ? c.uh64[j - 1] : widen64(c.uh[j - 1]));
 }
 __device__ inline long long up_f(const CombineDev& c, int j, int go, int ge) {
-  return j == 0 ? left_f64(c.border_up, c.rows_up, go, ge) : widen64(c.uf[j - 1]);
+  return j == 0 ? left_f64(c.border_up, c.rows_up, go, ge)
+                : (c.uf64 ? c.uf64[j - 1] : widen64(c.uf[j - 1]));
 }
 __device__ inline long long dn_h(const CombineDev& c, int q, int go, int ge) {
-  return q == 0 ? left_h64(c.border_dn, c.rows_dn, go, ge) : widen64(c.dh[q - 1]);
+  return q == 0 ? left_h64(c.border_dn, c.rows_dn, go, ge)
+                : (c.dh64 ? c.dh64[q - 1] : widen64(c.dh[q - 1]));
 }
 __device__ inline long long dn_f(const CombineDev& c, int q, int go, int ge) {
-  return q == 0 ? left_f64(c.border_dn, c.rows_dn, go, ge) : widen64(c.df[q - 1]);
+  return q == 0 ? left_f64(c.border_dn, c.rows_dn, go, ge)
+                : (c.df64 ? c.df64[q - 1] : widen64(c.df[q - 1]));
 }
 
 // One CTA per subproblem: max over hh/ff, then the first column attaining it.
@@ -457,6 +463,18 @@ extern "C" int32_t swb_crossings(swb_ctx* ctx, const swb_scheme* scheme, int32_t
   double ms = 0.0;
   rc = swb_run_passes(ctx, sc, reqs, &ms);
   if (rc) return rc;
+  for (int t = 0; t < n; ++t) {  // halves that ran on the int64 kernel
+    CombineDev& c = comb[t];
+    c.uh64 = c.uf64 = c.dh64 = c.df64 = nullptr;
+    if (reqs[2 * t].wide) {
+      c.uh64 = (const long long*)reqs[2 * t].fin64_h_dev;
+      c.uf64 = (const long long*)reqs[2 * t].fin64_f_dev;
+    }
+    if (reqs[2 * t + 1].wide) {
+      c.dh64 = (const long long*)reqs[2 * t + 1].fin64_h_dev;
+      c.df64 = (const long long*)reqs[2 * t + 1].fin64_f_dev;
+    }
+  }
   long long cells = 0;
   for (auto& r : reqs) cells += r.cells;
   if (cells_out) *cells_out = cells;

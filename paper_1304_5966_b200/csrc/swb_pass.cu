@@ -67,11 +67,16 @@ int swb_prepare_scheme(const swb_scheme* s, SchemeInt* out) {
   return SWB_OK;
 }
 
+// Dynamic range of a pass: real DP values lie in [-D, D]; sentinel-derived
+// ones in NEG32 +- D.
+static long long pass_range(const SchemeInt& sc, long long n1, long long n2) {
+  return (long long)sc.ge * (n1 + n2) + 2LL * sc.goe +
+         (long long)std::max(sc.max_sub, 0) * std::min(n1, n2) + 1024;
+}
+
 int swb_check_range(const SchemeInt& sc, long long n1, long long n2) {
-  // Real DP values lie in [-D, D]; sentinel-derived ones in NEG32 +- D.  Keep both
-  // inside their half of the int32 range (see SWB_NEG_REPORT).
-  const long long D = (long long)sc.ge * (n1 + n2) + 2LL * sc.goe +
-                      (long long)std::max(sc.max_sub, 0) * std::min(n1, n2) + 1024;
+  // Keep both inside their half of the int32 range (see SWB_NEG_REPORT).
+  const long long D = pass_range(sc, n1, n2);
   if (D >= (1LL << 28))
     return swb_fail(SWB_ERANGE,
                     "pass %lld x %lld with gap_extend %d / max_sub %d exceeds the int32 "
@@ -223,14 +228,16 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     order[q] = (int)q;
     PassReq& r = reqs[q];
     if (r.n1 < 1 || r.n2 < 1) return swb_fail(SWB_EINVAL, "cannot tile an empty matrix");
-    int rc = swb_check_range(sc, r.row_offset + r.n1, r.n2);
-    if (rc) return rc;
-    // tracked passes fold H and the row rank into one int32 key (H * 32 + rank)
-    if (r.track != kTrackNone &&
-        (long long)std::max(sc.max_sub, 0) * std::min<long long>(r.row_offset + r.n1, r.n2) +
-                sc.goe >= (1LL << 26) - 64)
-      return swb_fail(SWB_ERANGE, "tracked pass %d x %d exceeds the 26-bit score key range",
-                      r.n1, r.n2);
+    // Passes whose values do not fit the int32 kernels run on the int64 kernel
+    // (swb_wide.cu), as the reference computes in int64: the border ramps and
+    // scores (pass_range < 2^28) and, for tracked passes, the int32 key H * 32 +
+    // rank (max_sub * min(n1, n2) < 2^26).  Option "wide_log2" lowers both
+    // limits (tests drive every pass through the wide kernel with it).
+    const long long lim = 1LL << ctx->wide_log2;
+    r.wide = pass_range(sc, r.row_offset + r.n1, r.n2) >= lim ||
+             (r.track != kTrackNone &&
+              (long long)std::max(sc.max_sub, 0) * std::min<long long>(r.row_offset + r.n1, r.n2) +
+                      sc.goe >= (lim >> 2) - 64);
   }
   // packed 16x2 fast path eligibility (swb_x2.cuh header)
   // 95 max_sub <= 1021: 16-bit endpoint keys (swb_x2.cuh).  Window bound:
@@ -258,11 +265,29 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
   for (PassReq& r : reqs)
     r.x2 = x2_scheme && r.local && r.track == kTrackMin && !r.has_band &&
            r.prune <= 1 &&
+           // relative 16-bit frames: only the absolute H (boundary rows, running
+           // best) must fit int32, which the wide limit already guarantees when
+           // it is at its default
+           (!r.wide || (ctx->wide_log2 >= 28 &&
+                        ms * std::min<long long>(r.row_offset + r.n1, r.n2) < (1LL << 29))) &&
            // rows_per_lane forces the 32-bit kernel, except on row slabs where
            // it only fixes the strip granularity (64 x kX2SlabR rows here)
            (r.force_R == 0 || r.ext_in || r.ext_out) &&
            (!r.ext_out || r.n1 % (64 * kX2SlabR) == 0);  // slab bottom row = item bottom row
-  for (PassReq& r : reqs) r.x2_wild = r.x2 && sc.k == 5 && r.rows_code4;
+  for (PassReq& r : reqs) {
+    r.x2_wild = r.x2 && sc.k == 5 && r.rows_code4;
+    if (r.x2) r.wide = false;
+  }
+  // the wide passes leave the grouped launches and run on the int64 kernel
+  std::vector<PassReq*> wide;
+  {
+    std::vector<int> keep;
+    for (int q : order) {
+      if (reqs[q].wide) wide.push_back(&reqs[q]);
+      else keep.push_back(q);
+    }
+    order.swap(keep);
+  }
   // one launch per (recurrence, tracking, kernel) class; rows-per-lane per class
   auto cls = [&](int q) {
     return (reqs[q].x2_wild ? 200 : reqs[q].x2 ? 100 : 0) + (reqs[q].local ? 10 : 0) + reqs[q].track;
@@ -656,6 +681,12 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     }
     g0 = g1;
   }
+  if (!wide.empty()) {
+    double wms = 0.0;
+    const int rc = swb_run_wide(ctx, sc, wide, &wms);
+    if (rc) return rc;
+    if (kernel_ms_total) *kernel_ms_total += wms;
+  }
   return SWB_OK;
 }
 
@@ -775,6 +806,7 @@ extern "C" int64_t swb_get_option(swb_ctx* ctx, const char* name) {
   if (!strcmp(name, "live_ranges")) return ctx->live_ranges;
   if (!strcmp(name, "live_big")) return ctx->live_big;
   if (!strcmp(name, "watchdog_ms")) return ctx->watchdog_ms;
+  if (!strcmp(name, "wide_log2")) return ctx->wide_log2;
   if (!strcmp(name, "p2_R")) return ctx->p2_R;
   if (!strcmp(name, "mm_prune")) return ctx->mm_prune;
   if (!strcmp(name, "claim_mode")) return ctx->claim_mode;
@@ -823,6 +855,11 @@ extern "C" int32_t swb_set_option(swb_ctx* ctx, const char* name, int64_t value)
   }
   if (!strcmp(name, "p2_R")) {
     ctx->p2_R = (int)value;
+    return SWB_OK;
+  }
+  if (!strcmp(name, "wide_log2")) {
+    if (value < 4 || value > 28) return swb_fail(SWB_EINVAL, "wide_log2 must be in [4, 28]");
+    ctx->wide_log2 = (int)value;
     return SWB_OK;
   }
   if (!strcmp(name, "claim_log")) {
@@ -958,9 +995,17 @@ extern "C" int32_t swb_pass(swb_ctx* ctx, const swb_scheme* scheme, const swb_pa
     o.tiles_pruned = r.blocks_pruned;
     o.tiles_banded_out = std::max<long long>(0, r.blocks_total - r.blocks_exec - r.blocks_pruned);
     o.kernel_ms = r.kernel_ms;
-    o.kernel = r.x2 ? 1 : 0;
+    o.kernel = r.wide ? 2 : (r.x2 ? 1 : 0);
     o.rows_per_lane = r.R;
-    if (r.want_final) {
+    if (r.want_final && r.wide) {  // int64 kernel: the reference's values as they are
+      SWB_CUDA(cudaMemcpyAsync(d.final_row_h + 1, r.fin64_h_dev, sizeof(int64_t) * r.n2,
+                               cudaMemcpyDeviceToHost, ctx->stream));
+      SWB_CUDA(cudaMemcpyAsync(d.final_row_f + 1, r.fin64_f_dev, sizeof(int64_t) * r.n2,
+                               cudaMemcpyDeviceToHost, ctx->stream));
+      SWB_CUDA(cudaStreamSynchronize(ctx->stream));
+      d.final_row_h[0] = left_h_host(r.border, r.n1, sc.go, sc.ge);
+      d.final_row_f[0] = left_f_host(r.border, r.n1, sc.go, sc.ge);
+    } else if (r.want_final) {
       std::vector<int32_t> th(r.n2), tf(r.n2);
       SWB_CUDA(cudaMemcpyAsync(th.data(), r.fin_h_dev, sizeof(int32_t) * r.n2,
                                cudaMemcpyDeviceToHost, ctx->stream));

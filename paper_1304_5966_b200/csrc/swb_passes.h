@@ -54,6 +54,9 @@ struct PassReq {
   bool x2 = false;  // packed 16x2 phase-1 kernel
   bool rows_code4 = false;  // the row sequence holds code 4
   bool x2_wild = false;     // packed kernel with the constant-row wildcard (code 4)
+  bool wide = false;        // int64 kernel (swb_wide.cu): range beyond the int32 kernels
+  int64_t* fin64_h_dev = nullptr;  // wide passes: int64 final rows (device)
+  int64_t* fin64_f_dev = nullptr;
   int nstrips = 0;
   long long res_offset = 0;
   long long best_score = 0, best_i = -1, best_j = -1;
@@ -70,3 +73,7 @@ void swb_bind_maps(swb_ctx* ctx, PassReq* r, long long off1, long long len1, boo
                    long long offset);
 int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs,
                    double* kernel_ms_total);
+namespace swb {
+int swb_run_wide(swb_ctx* ctx, const SchemeInt& sc, const std::vector<PassReq*>& reqs,
+                 double* kernel_ms);
+}

@@ -305,6 +305,10 @@ def get_context(device: int = 0) -> DeviceContext:
         return ctx
 
 
+# swb_pass_out.kernel: which device kernel carried the pass
+KERNEL_NAMES = {0: "lane32", 1: "packed16x2", 2: "wide64"}
+
+
 @dataclass
 class PassResult:
     """engine.PassResult (engine.py:120-131); tiles replace 512x512 blocks."""
@@ -320,7 +324,7 @@ class PassResult:
     banded_out_blocks: int
     cells_executed: int
     kernel_ms: float = 0.0
-    kernel: str = "lane32"     # "lane32" or "packed16x2" (which kernel carried the pass)
+    kernel: str = "lane32"     # "lane32", "packed16x2" or "wide64" (KERNEL_NAMES)
     rows_per_lane: int = 0
 
 
@@ -432,7 +436,7 @@ class Session:
                 fin[0] if fin else None, fin[1] if fin else None,
                 int(o.tiles_total), int(o.tiles_executed), int(o.tiles_pruned),
                 int(o.tiles_banded_out), int(o.cells_executed), float(o.kernel_ms),
-                "packed16x2" if o.kernel == 1 else "lane32", int(o.rows_per_lane)))
+                KERNEL_NAMES.get(int(o.kernel), "lane32"), int(o.rows_per_lane)))
         # one launch carries all specs: count its time once
         if len(outs) > 1:
             self.kernel_ms -= sum(o.kernel_ms for o in outs[1:])
