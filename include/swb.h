@@ -237,7 +237,9 @@ int32_t swb_crossings(swb_ctx* ctx, const swb_scheme* scheme, int32_t seq1, int3
  * ops_out[ops_offsets[t] ...], capacity rows+cols; counts[t] = op count or -1
  * on a traceback dead end; scores[t] = achieved score (F or H at (rows, cols)
  * per end_vgap), SWB_NEG_INF_REF on a dead end.  Band per phase3.py:230-233
- * when band != 0, else the full rectangle. */
+ * when band == 1, the explicit (row - col) interval [prefix, suffix] of each
+ * subproblem when band == 2 (leaf_solve's lo / hi arguments, kernels.py:91),
+ * else the full rectangle. */
 int32_t swb_leaves(swb_ctx* ctx, const swb_scheme* scheme, int32_t seq1, int32_t seq2,
                    const swb_subproblem* leaves, int32_t n, int32_t band,
                    uint8_t* ops_out, const int64_t* ops_offsets, int64_t* counts,

@@ -563,7 +563,10 @@ extern "C" int32_t swb_leaves(swb_ctx* ctx, const swb_scheme* scheme, int32_t se
       d.svg = s.start_vgap;
       d.evg = s.end_vgap;
       long long lo, hi;
-      if (band) {
+      if (band == 2) {  // explicit interval (kernels.leaf_solve's lo / hi arguments)
+        lo = s.prefix;
+        hi = s.suffix;
+      } else if (band) {
         lo = mm_band_lo(rows, cols, s.expected, sc, &hi);
       } else {
         lo = -(rows + cols);
