@@ -325,7 +325,8 @@ def run_split_slabs_concurrent(S, world: int, leaf_limit: int | None = None, ban
                               leaf_limit or phase3.DEFAULT_LEAF_LIMIT, band, report)
 
 
-def split_align_distributed(seq1, seq2, scheme, config=None, report: dict | None = None):
+def split_align_distributed(seq1, seq2, scheme, config=None, report: dict | None = None,
+                            group=None):
     """AlignConfig(split=2) on all GPUs of a torch.distributed job (NCCL, one
     process per GPU): the paper's Figure-1 schedule.  Ranks [0, G/2) run the
     upper half as row slabs, ranks [G/2, G) the reversed lower half, all at
@@ -334,7 +335,9 @@ def split_align_distributed(seq1, seq2, scheme, config=None, report: dict | None
     memory.  Rank 0 receives the lower half's final row (the middle row) and
     the upper one over NCCL, merges the per-slab bests, max-reduces the tile
     maps, and finishes; every rank returns the same (summary, path), equal to
-    split_align on one GPU (reference split.py:84-182)."""
+    split_align on one GPU (reference split.py:84-182).  `group` (a
+    torch.distributed process group, default all ranks) lets several
+    alignments share one job (align_both_strands_distributed)."""
     import os
     import time
 
@@ -351,7 +354,8 @@ def split_align_distributed(seq1, seq2, scheme, config=None, report: dict | None
     if len(seq1) < 1 or len(seq2) < 1:
         raise ValueError("alignment inputs must be non-empty")
     scheme = validate_scheme(scheme)
-    rank, world = dist.get_rank(), dist.get_world_size()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    glob = (lambda r: dist.get_global_rank(group, r)) if group is not None else (lambda r: r)
     local = int(os.environ.get("LOCAL_RANK", cfg.device))
     torch.cuda.set_device(local)
     ctx = get_context(local)
@@ -373,7 +377,8 @@ def split_align_distributed(seq1, seq2, scheme, config=None, report: dict | None
         best = Boundary(ctx, 1) if rank == 0 else None
         handles = [None] * world
         dist.all_gather_object(handles, (inbound.export() if inbound else None,
-                                         ipc_export(ctx, best.progress) if best else None))
+                                         ipc_export(ctx, best.progress) if best else None),
+                              group=group)
         ext_out = None
         if feeds:
             hb, hp = handles[rank + 1][0]
@@ -381,7 +386,7 @@ def split_align_distributed(seq1, seq2, scheme, config=None, report: dict | None
         ext_in = (inbound.buf, inbound.progress) if inbound else None
         shared_best = best.progress if best else ipc_import(ctx, handles[0][1])
         try:
-            dist.barrier()
+            dist.barrier(group=group)
             res = None
             if me.slab.rows > 0:
                 ctx.set_option("rows_per_lane", SLAB_ROWS_PER_LANE)
@@ -392,7 +397,7 @@ def split_align_distributed(seq1, seq2, scheme, config=None, report: dict | None
             mine = (me.half, (res.best_score, res.best_i, res.best_j, res.cells_executed)
                     if res is not None else None)
             parts = [None] * world
-            dist.all_gather_object(parts, mine)
+            dist.all_gather_object(parts, mine, group=group)
             # the two final rows (int64 [n2 + 1] x 2 each) to rank 0 over NCCL
             finals = {}
             for half in ("up", "dn"):
@@ -404,9 +409,9 @@ def split_align_distributed(seq1, seq2, scheme, config=None, report: dict | None
                     buf.copy_(torch.from_numpy(np.stack([res.final_row_h, res.final_row_f])))
                 if owner != 0:
                     if rank == owner:
-                        dist.send(buf, dst=0)
+                        dist.send(buf, dst=glob(0), group=group)
                     elif rank == 0:
-                        dist.recv(buf, src=owner)
+                        dist.recv(buf, src=glob(owner), group=group)
                 if rank == 0:
                     h = buf.cpu().numpy()
                     finals[half] = (h[0].copy(), h[1].copy())
@@ -414,7 +419,7 @@ def split_align_distributed(seq1, seq2, scheme, config=None, report: dict | None
             for which in (1, 2):
                 ptr, n, _ = ctx.bounds_device(which)
                 full = torch.as_tensor(_DeviceRows(ptr, n), device=f"cuda:{local}")
-                dist.reduce(full, dst=0, op=dist.ReduceOp.MAX)
+                dist.reduce(full, dst=glob(0), op=dist.ReduceOp.MAX, group=group)
             torch.cuda.synchronize()
             out = [None]
             if rank == 0:
@@ -430,20 +435,101 @@ def split_align_distributed(seq1, seq2, scheme, config=None, report: dict | None
                     report.update(split_seconds=time.perf_counter() - t0, split_ranks=world)
                 out[0] = (summary.score, tuple(summary.start), tuple(summary.end),
                           tuple(path.start), path.ops.tobytes())
-            dist.broadcast_object_list(out, src=0)
+            dist.broadcast_object_list(out, src=glob(0), group=group)
         finally:
-            dist.barrier()
+            dist.barrier(group=group)
             if ext_out:
                 ctx.lib.swb_ipc_close(ctx.ptr, ext_out[0])
                 ctx.lib.swb_ipc_close(ctx.ptr, ext_out[1])
             if not best:
                 ctx.lib.swb_ipc_close(ctx.ptr, shared_best)
-            dist.barrier()
+            dist.barrier(group=group)
             if inbound:
                 inbound.free()
             if best:
                 best.free()
     sc, st, en, pst, ops = out[0]
+    if sc == 0:
+        return AlignmentSummary.empty(), AlignmentPath.empty()
+    return (AlignmentSummary(sc, Coord(*st), Coord(*en)),
+            AlignmentPath(Coord(*pst), np.frombuffer(ops, dtype=np.uint8).copy()))
+
+
+# -- both strands (§3: "four GPU cards in the case of aligning both
+#    strands") ------------------------------------------------------------------
+
+def reverse_complement_codes(codes, alphabet):
+    """Reverse complement of DNA codes over "ACGT" (+ the wildcard 'N', which
+    is its own complement)."""
+    import numpy as np
+    if alphabet.symbols[:4] != "ACGT" or len(alphabet) > 5:
+        raise ValueError("both-strand alignment needs a DNA alphabet (ACGT, optionally N)")
+    comp = np.array([3, 2, 1, 0, 4], dtype=np.uint8)
+    return comp[np.asarray(codes, dtype=np.uint8)[::-1]]
+
+
+def strand_groups(world: int) -> tuple[list[int], list[int]]:
+    """Ranks aligning the forward and the reverse-complement strand."""
+    if world < 2:
+        raise ValueError("both strands across GPUs need at least 2 ranks")
+    half = world // 2
+    return list(range(half)), list(range(half, world))
+
+
+def align_both_strands(seq1, seq2, scheme, config=None):
+    """seq1 against seq2 and against the reverse complement of seq2 (one GPU,
+    one after the other).  Returns {"+": (summary, path), "-": (summary,
+    path)}; the "-" coordinates index the reverse-complemented seq2."""
+    from .model import Sequence
+    from .pipeline import align
+    rc = Sequence.from_codes(seq2.id + "_rc", reverse_complement_codes(seq2.codes, scheme.alphabet),
+                             scheme.alphabet)
+    return {"+": align(seq1, seq2, scheme, config), "-": align(seq1, rc, scheme, config)}
+
+
+def align_both_strands_distributed(seq1, seq2, scheme, config=None):
+    """Both strands on all GPUs of a torch.distributed job: ranks [0, G/2)
+    align the forward strand, [G/2, G) the reverse complement, each half with
+    the Figure-1 split across its own two GPU groups when it has >= 2 ranks
+    (split_align_distributed on a sub-group; 4 GPUs = the paper's four-card
+    case), else on its one GPU.  Every rank returns the same
+    {"+": (summary, path), "-": (summary, path)}."""
+    import os
+
+    import torch.distributed as dist
+
+    from .engine import get_context
+    from .model import Sequence
+    from .pipeline import AlignConfig, align
+
+    cfg = config or AlignConfig(split=2)
+    rank, world = dist.get_rank(), dist.get_world_size()
+    if world < 2:
+        return align_both_strands(seq1, seq2, scheme, cfg)
+    fwd, rev = strand_groups(world)
+    groups = [dist.new_group(fwd), dist.new_group(rev)]  # every rank creates both
+    mine = 0 if rank in fwd else 1
+    ranks = fwd if mine == 0 else rev
+    s2 = seq2 if mine == 0 else Sequence.from_codes(
+        seq2.id + "_rc", reverse_complement_codes(seq2.codes, scheme.alphabet), scheme.alphabet)
+    local = int(os.environ.get("LOCAL_RANK", cfg.device))
+    get_context(local)
+    if len(ranks) >= 2:
+        res = split_align_distributed(seq1, s2, scheme, AlignConfig(
+            leaf_limit=cfg.leaf_limit, band=cfg.band, split=2, device=local), group=groups[mine])
+    else:
+        res = align(seq1, s2, scheme, AlignConfig(leaf_limit=cfg.leaf_limit, band=cfg.band,
+                                                  split=cfg.split, device=local))
+    out = [None] * world
+    dist.all_gather_object(out, (mine, (res[0].score, tuple(res[0].start), tuple(res[0].end),
+                                        tuple(res[1].start), res[1].ops.tobytes())))
+    return {("+" if m == 0 else "-"): _unpack(r) for m, r in (out[fwd[0]], out[rev[0]])}
+
+
+def _unpack(r):
+    import numpy as np
+    from .model import AlignmentPath, AlignmentSummary, Coord
+    sc, st, en, pst, ops = r
     if sc == 0:
         return AlignmentSummary.empty(), AlignmentPath.empty()
     return (AlignmentSummary(sc, Coord(*st), Coord(*en)),

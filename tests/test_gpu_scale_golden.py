@@ -152,3 +152,20 @@ def test_c4_window_score():
     g = GOLDEN["C4w"]
     r = swb.score_only(s1, s2, SCHEME)
     assert (r.score, list(r.end)) == (g["score"], g["end"])
+
+
+def test_both_strands_single_gpu():
+    """align_both_strands finds an inverted copy on the minus strand and
+    equals align() on (seq1, seq2) and (seq1, revcomp(seq2))."""
+    from paper_1304_5966_b200.multigpu import align_both_strands, reverse_complement_codes
+    a, b = synthetic_pair(60_000, seed=77)
+    b = np.concatenate([b[:20_000], reverse_complement_codes(a[30_000:50_000], SCHEME.alphabet)])
+    s1 = Sequence.from_codes("t", a, SCHEME.alphabet)
+    s2 = Sequence.from_codes("q", b, SCHEME.alphabet)
+    both = align_both_strands(s1, s2, SCHEME)
+    fwd = swb.align(s1, s2, SCHEME)
+    rc = Sequence.from_codes("q_rc", reverse_complement_codes(b, SCHEME.alphabet), SCHEME.alphabet)
+    rev = swb.align(s1, rc, SCHEME)
+    assert both["+"][0] == fwd[0] and np.array_equal(both["+"][1].ops, fwd[1].ops)
+    assert both["-"][0] == rev[0] and np.array_equal(both["-"][1].ops, rev[1].ops)
+    assert both["-"][0].score >= 19_000  # the inverted 20 kbp copy, exact

@@ -193,3 +193,13 @@ def test_split_plan_shapes():
     small = split_plan(900, 8, strip_rows=1024)  # fewer strips than ranks: trailing ranks idle
     assert [hs.slab.rows for hs in small] == [450, 0, 0, 0, 450, 0, 0, 0]
     assert [hs.last for hs in small] == [True, False, False, False, True, False, False, False]
+
+
+def test_reverse_complement_and_strand_groups():
+    from paper_1304_5966_b200 import Alphabet
+    from paper_1304_5966_b200.multigpu import reverse_complement_codes, strand_groups
+    codes = np.array([0, 1, 2, 3, 4, 0], dtype=np.uint8)  # A C G T N A
+    assert reverse_complement_codes(codes, Alphabet.dna()).tolist() == [3, 4, 0, 1, 2, 3]
+    assert strand_groups(4) == ([0, 1], [2, 3]) and strand_groups(2) == ([0], [1])
+    with pytest.raises(ValueError):
+        reverse_complement_codes(codes, Alphabet.protein())
