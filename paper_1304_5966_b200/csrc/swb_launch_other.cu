@@ -17,7 +17,6 @@ template <int TRACK>
 int dispatch_other_T(swb_ctx* ctx, int R, const PassParams* P, long long items, int ctas_per_sm,
                      int* occ_out) {
   switch (R) {
-    case 2: return dispatch_other_R<2, TRACK>(ctx, P, items, ctas_per_sm, occ_out);
     case 8: return dispatch_other_R<8, TRACK>(ctx, P, items, ctas_per_sm, occ_out);
     case 16: return dispatch_other_R<16, TRACK>(ctx, P, items, ctas_per_sm, occ_out);
     case 24: return dispatch_other_R<24, TRACK>(ctx, P, items, ctas_per_sm, occ_out);

@@ -140,6 +140,7 @@ Shape choose_shape(swb_ctx* ctx, const std::vector<PassReq*>& jobs, bool local, 
   double best_t = 1e300;
   for (int q = 0; q < ncand; ++q) {
     const int R = cand[q];
+    if (R < ctx->min_R) continue;
     int occ = 0;
     const int rc = x2    ? dispatch_x2(ctx, R, nullptr, 0, 0, &occ, false, x2f)
                    : big ? dispatch_big(ctx, R, nullptr, 0, local, track, 0, &occ)
@@ -855,6 +856,10 @@ extern "C" int32_t swb_set_option(swb_ctx* ctx, const char* name, int64_t value)
   }
   if (!strcmp(name, "p2_R")) {
     ctx->p2_R = (int)value;
+    return SWB_OK;
+  }
+  if (!strcmp(name, "min_R")) {
+    ctx->min_R = (int)value;
     return SWB_OK;
   }
   if (!strcmp(name, "wide_log2")) {
