@@ -111,7 +111,7 @@ struct JobDev {
   const int32_t* rmap_rev;
   int2* alive;             // per strip (live lo + 1, live hi + 1), 0 = unset (restricted passes)
   int32_t live_mode;       // bit 0: late start, bit 1: early exit
-  int32_t best_sys;        // prune_best is shared across slabs / GPUs: system-scope access
+  int32_t best_sys;        // prune_best is shared across slabs / GPUs (informational)
   int4* bmap_live;         // writer: per row tile (-(lo+1), hi, covered) of the columns it swept
   const int4* rmap_live;   // reader: unwritten reverse-map tiles outside that interval are fill
   int32_t bin_rev;         // bmap_in is the reverse map (rmap_live applies to it)
@@ -139,6 +139,8 @@ struct PassParams {
   int32_t chunk;            // > 0: CTA claims `chunk` consecutive strips (item_map: job, first)
   int32_t big;              // substitution table mode (tab) instead of tlo/thi
   const int32_t* tab;       // 32 x 33 table, device (big schemes)
+  int32_t defer_pub;              // packed kernel: release each block's progress one block late
+  int32_t pad_pp;
   unsigned long long launch_id;   // diagnostics: context launch counter at this launch
   unsigned long long* claim_log;  // diagnostics ring (claim_log in swb_kernels.cuh) or null
   unsigned long long* strip_dbg;  // per strip (item_base + s) 8 words: ranges, exit,
@@ -233,15 +235,14 @@ __device__ __forceinline__ int ld_relaxed(const int32_t* p) {
   return v;
 }
 
-// running best for pruning: per pass (gpu scope) or shared between the row
-// slabs of a pass, possibly on other GPUs (system scope, swb_pass_desc.shared_best)
-__device__ __forceinline__ int load_best(const JobDev& J) {
-  return J.best_sys ? ld_relaxed_sys(J.prune_best) : ld_relaxed(J.prune_best);
-}
-__device__ __forceinline__ void raise_best(const JobDev& J, int v) {
-  if (J.best_sys) atomicMax_system(J.prune_best, v);
-  else atomicMax(J.prune_best, v);
-}
+// Running best for pruning: a pass's own word, or one word shared by the row
+// slabs of a pass (swb_pass_desc.shared_best), possibly in a peer GPU's memory.
+// GPU-scope accesses serve both: the value is a stale-only hint (any value once
+// written is a real cell score), the reduction is atomic at the word's home L2
+// whichever GPU issues it, and a branch on the scope here measured 1-2 % of a
+// C2 pass (the hot kernels issue these every 32-column block).
+__device__ __forceinline__ int load_best(const JobDev& J) { return ld_relaxed(J.prune_best); }
+__device__ __forceinline__ void raise_best(const JobDev& J, int v) { atomicMax(J.prune_best, v); }
 
 // Spin until *p >= need with exponential back-off: a waiting warp shares its
 // SM sub-partition with a computing one, so it must not steal issue slots;
@@ -827,10 +828,12 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     // The column codes were prefetched one block ahead; the producer's
     // progress is polled only when the last observed value does not cover
     // this block, and acquired with one ld.acquire.
+    // running best: every lane loads it (stale-only, any lane's value is
+    // sound); the skip / tracking decisions below are made warp-uniform by votes
+    if (LOCAL && J.prune == 1) prune_seen = load_best(J);
     {
       const int c = s0 + lane;
       const int code = code_next;
-      const int pb_now = (LOCAL && J.prune == 1 && lane == 0) ? load_best(J) : 0;
       {
         const int cn = c + 32;
         code_next = (cn < ce) ? (int)J.cols[SWB_IX((long long)cn * J.cstep, (long long)n2 * J.cstep)] : 0;
@@ -913,7 +916,6 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       // pair its shuffles with theirs (shfl.sync matches any shfl.sync of the
       // same mask).  Lane 0's running best is as stale-safe as any; a known
       // live end is final, so the minimum over lanes adopts it.
-      prune_seen = __shfl_sync(0xffffffffu, pb_now, 0);
       if (dyn) ahi_p = __reduce_min_sync(0xffffffffu, ahi_p);
       __syncwarp();  // ring stores visible to the steps
     }
@@ -956,9 +958,11 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       const long long ms = P.max_sub;
       if (J.prune == 1) {
         const long long bound = (inm > 0 ? inm : 0) + ms * (long long)(rem_r < rem_c ? rem_r : rem_c);
-        skip = bound < (long long)prune_seen;
+        // votes keep both decisions warp-uniform (each lane's best is sound)
+        skip = __any_sync(0xffffffffu, bound < (long long)prune_seen);
         // a path inside the 63-column-wide skewed block gains <= 63 * max_sub
-        track_block = (inm > 0 ? inm : 0) + 63LL * ms >= (long long)prune_seen;
+        track_block = __any_sync(0xffffffffu,
+                                 (inm > 0 ? inm : 0) + 63LL * ms >= (long long)prune_seen);
       } else if (J.prune == 2) {
         const long long bound = inm + ms * (long long)(rem_r < rem_c ? rem_r : rem_c);
         skip = bound < (long long)J.prune_target;

@@ -537,6 +537,7 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     if (!d_sdbg) return swb_fail(SWB_ECUDA, "out of device memory (strip diagnostics)");
     P.strip_dbg = d_sdbg;
     P.launch_id = (unsigned long long)ctx->launches;
+    P.defer_pub = ctx->x2_defer;
     if (ctx->claim_log_on) {
       if (!ctx->claim_log.p) {
         if (!swb_scratch(ctx->claim_log, 8 * (8 + 4 * 4096))) return swb_fail(SWB_ECUDA, "claim log");
@@ -808,6 +809,7 @@ extern "C" int64_t swb_get_option(swb_ctx* ctx, const char* name) {
   if (!strcmp(name, "live_big")) return ctx->live_big;
   if (!strcmp(name, "watchdog_ms")) return ctx->watchdog_ms;
   if (!strcmp(name, "wide_log2")) return ctx->wide_log2;
+  if (!strcmp(name, "x2_defer")) return ctx->x2_defer;
   if (!strcmp(name, "p2_R")) return ctx->p2_R;
   if (!strcmp(name, "mm_prune")) return ctx->mm_prune;
   if (!strcmp(name, "claim_mode")) return ctx->claim_mode;
@@ -856,6 +858,10 @@ extern "C" int32_t swb_set_option(swb_ctx* ctx, const char* name, int64_t value)
   }
   if (!strcmp(name, "p2_R")) {
     ctx->p2_R = (int)value;
+    return SWB_OK;
+  }
+  if (!strcmp(name, "x2_defer")) {
+    ctx->x2_defer = (int)value;
     return SWB_OK;
   }
   if (!strcmp(name, "min_R")) {

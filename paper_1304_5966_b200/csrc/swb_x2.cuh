@@ -203,6 +203,8 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
   }
 
   int known_prog = 0, prune_seen = 0, published = 0;
+  const bool defer = P.defer_pub && !ext_out;
+  int pending_pub = 0;
   int code_next = (lane < n2) ? (int)J.cols[(long long)lane * J.cstep] : 0;
   long long pruned_blocks = 0, exec_blocks = 0, wait_cycles = 0;
   const long long t_strip0 = clock64();
@@ -290,10 +292,16 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     //     the profile window and stage the new columns' words
     const int c = s0 + lane;
     int top_h = -goe, top_f = SWB_NEG32;  // local top border: H = 0, F = -inf
+    // The running best also decides tracking, so it is kept with pruning off.
+    // It steers skip / tracking around the shuffling steps, so it must be the
+    // same in every lane (a lane that skipped while the others ran would pair
+    // its shuffles with theirs): the warp reconverges and loads it with ONE
+    // warp-wide load of one address, which returns one value to all lanes.
+    // (A broadcast or vote here measured 3-4 % slower on C2.)
+    __syncwarp();
+    prune_seen = load_best(J);
     {
       const int code = code_next;
-      // the running best also decides tracking, so it is kept with pruning off
-      const int pb_now = lane == 0 ? load_best(J) : 0;
       {
         const int cn = c + 32;
         code_next = (cn < n2) ? (int)J.cols[(long long)cn * J.cstep] : 0;
@@ -323,8 +331,6 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
       sm->prof[lane] = p1;
       sm->prof[32 + lane] = p2;
       sm->prof[64 + lane] = c < n2 ? tw_s[code] : 0u;
-      // warp-uniform: it steers skip / tracking around the shuffling steps
-      prune_seen = __shfl_sync(0xffffffffu, pb_now, 0);
     }
 
     // (1b) re-base: warp maximum over the state and the incoming top row
@@ -497,8 +503,16 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     }
     __syncwarp();
 
-    // (4) flush B's bottom row for columns [s0 - 63, s0 - 31) and publish
+    // (4) flush B's bottom row for columns [s0 - 63, s0 - 31) and publish.
+    // Deferred publication (P.defer_pub): the progress covering the PREVIOUS
+    // block is released before this block's stores, so the release's fence
+    // finds that block's stores long complete instead of stalling on the ones
+    // just issued; consumers trail by one more block.
     {
+      if (defer) {
+        if (lane == 0 && pending_pub > 0) st_release(my_progress, pending_pub);
+        __syncwarp();
+      }
       const int cf = s0 - 63 + lane;
       if (cf >= 0 && cf < n2) {
         int2 o = make_int2(-goe, SWB_NEG32);  // pruned block: the fill values
@@ -511,13 +525,13 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
       }
       if (ext_out) __threadfence_system();
       __syncwarp();
-      if (lane == 0) {
-        int pub = s0 - 31;
-        if (pub > n2) pub = n2;
-        if (pub > 0) {
-          if (ext_out) st_release_sys(my_progress, pub);
-          else st_release(my_progress, pub);
-        }
+      int pub = s0 - 31;
+      if (pub > n2) pub = n2;
+      if (defer) {
+        pending_pub = pub;
+      } else if (lane == 0 && pub > 0) {
+        if (ext_out) st_release_sys(my_progress, pub);
+        else st_release(my_progress, pub);
       }
     }
 
@@ -583,10 +597,6 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
     J.strip_times[3 * s + 0] = g0;
     J.strip_times[3 * s + 1] = g1;
-    P.strip_dbg[8 * (J.item_base + s) + 0] = (unsigned)n2;
-    P.strip_dbg[8 * (J.item_base + s) + 1] = ((unsigned long long)(unsigned)n2 << 32) | 0xffffffffu;
-    P.strip_dbg[8 * (J.item_base + s) + 2] = ((unsigned long long)exec_blocks << 32) | (unsigned long long)pruned_blocks;
-    P.strip_dbg[8 * (J.item_base + s) + 3] = 0;
     J.strip_times[3 * s + 2] = P.proto == 10 ? g_diag : gw;  // proto 10: diagonal entry time
   }
 }

@@ -1,2 +1,3 @@
 export SWB_WATCHDOG_MS=120000
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_scale_golden.py -q -x -k "groups or split" > gpurun_out/f1s.log 2>&1; echo rc=$? >> gpurun_out/f1s.log
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/t6.log 2>&1; echo rc=$? >> gpurun_out/t6.log
+timeout 600 python tools/option_ab.py 5000000 x2 1 2 > gpurun_out/c3_6.log 2>&1
