@@ -1238,8 +1238,9 @@ __global__ void __launch_bounds__(256) pass_kernel(const PassParams P) {
   const int lane = threadIdx.x & 31;
   WarpSmem* sm = &wsm[warp];
   if (P.chunk > 0) {
-    // chain chunks: 128 threads, warp w runs strip first + w of the claimed chunk
-    __shared__ ChainChan chan[4];
+    // chain chunks: 32 x P.chunk threads (4 or 8 warps), warp w runs strip
+    // first + w of the claimed chunk
+    __shared__ ChainChan chan[8];
     for (;;) {
       if (threadIdx.x == 0) base_s = (long long)atomicAdd(P.claim, 1ULL);
       if (lane == 0) {
@@ -1254,7 +1255,7 @@ __global__ void __launch_bounds__(256) pass_kernel(const PassParams P) {
       const int s = m.y + warp;
       if (s < J.nstrips) {
         ChainChan* cin = (warp > 0) ? &chan[warp - 1] : nullptr;
-        ChainChan* cout = (warp < 3 && s + 1 < J.nstrips) ? &chan[warp] : nullptr;
+        ChainChan* cout = (warp < P.chunk - 1 && s + 1 < J.nstrips) ? &chan[warp] : nullptr;
         run_chunk_strip<R, LOCAL, TRACK, BIG>(P, J, s, sm, tlo_s, thi_s, cin, cout);
       }
       __syncthreads();

@@ -77,7 +77,13 @@ int launch_any(swb_ctx* ctx, K kern, const PassParams& Pin, long long items, int
   if (P.chunk > 0) {
     const long long cap = (long long)per_sm * ctx->sms;
     const int grid = (int)std::min(cap, std::max((long long)P.total_items, 1LL));
-    kern<<<grid, 128, 0, ctx->stream>>>(P);
+    int per = per_sm;
+    if (P.chunk > 4) {  // 8-warp chunks: occupancy of the wider CTA
+      SWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 32 * P.chunk, 0));
+      if (per < 1) return swb_fail(SWB_ECUDA, "chunk CTA does not fit on an SM");
+    }
+    const int grid2 = (int)std::min((long long)per * ctx->sms, std::max((long long)P.total_items, 1LL));
+    kern<<<P.chunk > 4 ? grid2 : grid, 32 * P.chunk, 0, ctx->stream>>>(P);
     ctx->launches++;
     SWB_CUDA(cudaGetLastError());
     return SWB_OK;

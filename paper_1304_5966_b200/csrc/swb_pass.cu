@@ -484,7 +484,7 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
       d_map = A.take<int2>(total_strips);
       int max_strips = 0;
       for (int t = 0; t < nj; ++t) max_strips = std::max(max_strips, h_jobs[t].nstrips);
-      for (int st = 0; st < max_strips; st += 4)
+      for (int st = 0; st < max_strips; st += ctx->chain_chunk)
         for (int t = 0; t < nj; ++t)
           if (st < h_jobs[t].nstrips) h_map[chunk_items++] = make_int2(t, st);
     } else if (nj > 1 && !ctx->job_major) {  // (group-mode launches drop it, see launch_any)
@@ -552,7 +552,7 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
       if (reqs[order[t]].rmap_fwd) P.warp_claim = 1;
     P.chain_wait = P.warp_claim && ctx->chain_wait;
     if (chain_chunks) {
-      P.chunk = 4;
+      P.chunk = ctx->chain_chunk;
       P.total_items = chunk_items;
     }
     memcpy(P.tlo, sc.tlo, sizeof(P.tlo));
@@ -810,6 +810,7 @@ extern "C" int64_t swb_get_option(swb_ctx* ctx, const char* name) {
   if (!strcmp(name, "watchdog_ms")) return ctx->watchdog_ms;
   if (!strcmp(name, "wide_log2")) return ctx->wide_log2;
   if (!strcmp(name, "x2_defer")) return ctx->x2_defer;
+  if (!strcmp(name, "chain_chunk")) return ctx->chain_chunk;
   if (!strcmp(name, "p2_R")) return ctx->p2_R;
   if (!strcmp(name, "mm_prune")) return ctx->mm_prune;
   if (!strcmp(name, "claim_mode")) return ctx->claim_mode;
@@ -858,6 +859,11 @@ extern "C" int32_t swb_set_option(swb_ctx* ctx, const char* name, int64_t value)
   }
   if (!strcmp(name, "p2_R")) {
     ctx->p2_R = (int)value;
+    return SWB_OK;
+  }
+  if (!strcmp(name, "chain_chunk")) {
+    if (value != 4 && value != 8) return swb_fail(SWB_EINVAL, "chain_chunk must be 4 or 8");
+    ctx->chain_chunk = (int)value;
     return SWB_OK;
   }
   if (!strcmp(name, "x2_defer")) {
