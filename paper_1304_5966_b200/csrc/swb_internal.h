@@ -55,6 +55,8 @@ struct swb_ctx {
   // tile bound maps of one sequence pair
   int bmap_seq1 = -1, bmap_seq2 = -1;
   int bmap_nr = 0, bmap_nc = 0;
+  int bmap_shift = 10;          // tile edge 2^bmap_shift of the current maps
+  int map_shift = 10;           // option map_tile_log2: edge of the next maps
   int bmaps_on = 1;             // option "bound_maps": 0 disables reads and writes
   int live_ranges = 3;  // restricted passes: bit 0 late start, bit 1 early exit
   int claim_log_on = 0; // option claim_log: record claims in a device ring (swb_debug_claims)

@@ -115,7 +115,7 @@ struct JobDev {
   int4* bmap_live;         // writer: per row tile (-(lo+1), hi, covered) of the columns it swept
   const int4* rmap_live;   // reader: unwritten reverse-map tiles outside that interval are fill
   int32_t bin_rev;         // bmap_in is the reverse map (rmap_live applies to it)
-  int32_t pad5;
+  int32_t map_shift;       // log2 of the tile edge (10: 1024 x 1024 tiles)
 };
 
 static_assert(sizeof(JobDev) % 16 == 0, "JobDev arrays are staged next to int4 data");
@@ -281,7 +281,6 @@ __device__ __forceinline__ void wait_progress(const int32_t* p, int need, bool s
 // bound of its H values (every block contributes max(inputs) + W max_sub, an
 // upper bound of every cell it covers), and a later pass may skip a block
 // when even the best continuation the map allows cannot reach its target.
-constexpr int kTileShift = 10;
 constexpr long long kBoundEnc = 1LL << 30;
 
 __device__ __forceinline__ int bound_enc(long long v) {
@@ -290,7 +289,7 @@ __device__ __forceinline__ int bound_enc(long long v) {
 }
 
 // forward tile range [lo, hi] of pass rows (or columns) [a, b], a <= b
-__device__ __forceinline__ void tile_range(int base, int dir, int a, int b, int ntiles,
+__device__ __forceinline__ void tile_range(int base, int dir, int a, int b, int ntiles, int shift,
                                            int& lo, int& hi) {
   int fa = base + dir * a, fb = base + dir * b;
   if (fa > fb) {
@@ -298,8 +297,8 @@ __device__ __forceinline__ void tile_range(int base, int dir, int a, int b, int 
     fa = fb;
     fb = t;
   }
-  lo = fa < 0 ? 0 : (fa >> kTileShift);
-  hi = fb < 0 ? 0 : (fb >> kTileShift);
+  lo = fa < 0 ? 0 : (fa >> shift);
+  hi = fb < 0 ? 0 : (fb >> shift);
   if (lo > ntiles - 1) lo = ntiles - 1;
   if (hi > ntiles - 1) hi = ntiles - 1;
 }
@@ -370,7 +369,7 @@ __device__ __forceinline__ bool map_unknown(const JobDev& J, int raw, int rt, in
   const int4 e = J.rmap_live[SWB_IX(rt, J.map_nr)];
   if (!e.z) return true;
   const int lo = -e.x - 1, hi = e.y;
-  const int t0 = ct << kTileShift, t1 = t0 + (1 << kTileShift) - 1;
+  const int t0 = ct << J.map_shift, t1 = t0 + (1 << J.map_shift) - 1;
   return !(t1 < lo || t0 > hi);
 }
 
@@ -466,8 +465,8 @@ __device__ __forceinline__ void static_range(const JobDev& J, int s, int& cb, in
   const int r0 = s * 32 * R;
   const int r1 = (r0 + 32 * R < J.n1 ? r0 + 32 * R : J.n1) - 1;
   int rt_lo, rt_hi, ct_lo, ct_hi;
-  tile_range(J.map_r0, J.map_rdir, r0, r1, J.map_nr, rt_lo, rt_hi);
-  tile_range(J.map_c0, J.map_cdir, cb, ce - 1, J.map_nc, ct_lo, ct_hi);
+  tile_range(J.map_r0, J.map_rdir, r0, r1, J.map_nr, J.map_shift, rt_lo, rt_hi);
+  tile_range(J.map_c0, J.map_cdir, cb, ce - 1, J.map_nc, J.map_shift, ct_lo, ct_hi);
   int fmin = 0x7fffffff, fmax = -1;
   for (int base = ct_lo; base <= ct_hi; base += 32) {
     const int ct = base + lane;
@@ -493,7 +492,7 @@ __device__ __forceinline__ void static_range(const JobDev& J, int s, int& cb, in
     ce = cb;
     return;
   }
-  const long long flo = (long long)fmin << kTileShift, fhi = (((long long)fmax + 1) << kTileShift) - 1;
+  const long long flo = (long long)fmin << J.map_shift, fhi = (((long long)fmax + 1) << J.map_shift) - 1;
   long long lo, hi;  // pass columns
   if (J.map_cdir > 0) {
     lo = flo - J.map_c0;
@@ -640,7 +639,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
   if (cb >= ce) {
     if (dyn && J.bmap_live && J.bmap_out && lane == 0) {
       int rl, rh;
-      tile_range(J.map_r0, J.map_rdir, R0, (R0 + 32 * R < n1 ? R0 + 32 * R : n1) - 1, J.map_nr, rl, rh);
+      tile_range(J.map_r0, J.map_rdir, R0, (R0 + 32 * R < n1 ? R0 + 32 * R : n1) - 1, J.map_nr, J.map_shift, rl, rh);
       live_record(J, rl, rh, 1, 0);  // covered, nothing swept
     }
     if (lane == 0) {
@@ -670,9 +669,9 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
   BoundReader brd;
   if (J.bmap_out) {
     const int r_hi = (R0 + 32 * R < n1 ? R0 + 32 * R : n1) - 1;
-    tile_range(J.map_r0, J.map_rdir, R0, r_hi, J.map_nr, bw.rt_lo, bw.rt_hi);
+    tile_range(J.map_r0, J.map_rdir, R0, r_hi, J.map_nr, J.map_shift, bw.rt_lo, bw.rt_hi);
   }
-  if (J.bmap_in) tile_range(J.map_r0, J.map_rdir, R0 - 1, R0 + 32 * R, J.map_nr, brd.rt_lo, brd.rt_hi);
+  if (J.bmap_in) tile_range(J.map_r0, J.map_rdir, R0 - 1, R0 + 32 * R, J.map_nr, J.map_shift, brd.rt_lo, brd.rt_hi);
 
   // Row codes -> PRMT selectors (byte a, sign replicated into bytes 1..3).
   uint32_t sel[R];
@@ -990,7 +989,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
     // the map allows cannot reach the target; record this block's bound
     if (J.bmap_in && prunable && !skip) {
       int ta, tb;
-      tile_range(J.map_c0, J.map_cdir, s0 - 32, s0 + 32, J.map_nc, ta, tb);
+      tile_range(J.map_c0, J.map_cdir, s0 - 32, s0 + 32, J.map_nc, J.map_shift, ta, tb);
       const long long mx = br_get(J, brd, ta, tb, lane);
       if (mx != LLONG_MAX &&
           inm + 63LL * P.max_sub + mx + J.bound_offset < (long long)J.prune_target)
@@ -1001,7 +1000,7 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
       const int hi = s0 + 31 < ce - 1 ? s0 + 31 : ce - 1;
       if (lo <= hi) {
         int ta, tb;
-        tile_range(J.map_c0, J.map_cdir, lo, hi, J.map_nc, ta, tb);
+        tile_range(J.map_c0, J.map_cdir, lo, hi, J.map_nc, J.map_shift, ta, tb);
         bw_add(J, bw, ta, tb, (LOCAL && inm < 0 ? 0 : inm) + 63LL * P.max_sub, lane);
       }
     }

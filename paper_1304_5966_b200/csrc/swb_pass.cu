@@ -428,6 +428,7 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
       J.bmap_in = r.bmap_in;
       J.map_nr = r.map_nr;
       J.map_nc = r.map_nc;
+      J.map_shift = r.map_shift;
       J.map_r0 = r.map_r0;
       J.map_rdir = r.map_rdir;
       J.map_c0 = r.map_c0;
@@ -724,6 +725,7 @@ void swb_bind_maps(swb_ctx* ctx, PassReq* r, long long off1, long long len1, boo
   int32_t* rev = reinterpret_cast<int32_t*>(ctx->bmap_rev.p);
   r->map_nr = ctx->bmap_nr;
   r->map_nc = ctx->bmap_nc;
+  r->map_shift = ctx->bmap_shift;
   r->map_r0 = (int)(rev1 ? off1 + len1 - 1 : off1);
   r->map_rdir = rev1 ? -1 : 1;
   r->map_c0 = (int)(rev2 ? off2 + len2 - 1 : off2);
@@ -742,8 +744,9 @@ extern "C" int32_t swb_bounds_reset(swb_ctx* ctx, int32_t seq1, int32_t seq2) {
   if (seq1 < 0 || seq1 >= (int)ctx->seqs.size() || !ctx->seqs[seq1].live || seq2 < 0 ||
       seq2 >= (int)ctx->seqs.size() || !ctx->seqs[seq2].live)
     return swb_fail(SWB_EINVAL, "bad sequence id");
-  const long long nr = std::max<long long>(1, (ctx->seqs[seq1].n + 1023) >> 10);
-  const long long nc = std::max<long long>(1, (ctx->seqs[seq2].n + 1023) >> 10);
+  const int sh = ctx->map_shift;  // tile edge 2^sh (option map_tile_log2)
+  const long long nr = std::max<long long>(1, (ctx->seqs[seq1].n + (1LL << sh) - 1) >> sh);
+  const long long nc = std::max<long long>(1, (ctx->seqs[seq2].n + (1LL << sh) - 1) >> sh);
   const size_t bytes = sizeof(int32_t) * (size_t)nr * (size_t)nc;
   void* f = swb_scratch(ctx->bmap_fwd, bytes);
   void* r = f ? swb_scratch(ctx->bmap_rev, bytes) : nullptr;
@@ -763,6 +766,7 @@ extern "C" int32_t swb_bounds_reset(swb_ctx* ctx, int32_t seq1, int32_t seq2) {
   ctx->bmap_seq2 = seq2;
   ctx->bmap_nr = (int)nr;
   ctx->bmap_nc = (int)nc;
+  ctx->bmap_shift = sh;
   SWB_API_END();
 }
 
@@ -811,6 +815,7 @@ extern "C" int64_t swb_get_option(swb_ctx* ctx, const char* name) {
   if (!strcmp(name, "wide_log2")) return ctx->wide_log2;
   if (!strcmp(name, "x2_defer")) return ctx->x2_defer;
   if (!strcmp(name, "chain_chunk")) return ctx->chain_chunk;
+  if (!strcmp(name, "map_tile_log2")) return ctx->bmap_seq1 >= 0 ? ctx->bmap_shift : ctx->map_shift;
   if (!strcmp(name, "p2_R")) return ctx->p2_R;
   if (!strcmp(name, "mm_prune")) return ctx->mm_prune;
   if (!strcmp(name, "claim_mode")) return ctx->claim_mode;
@@ -859,6 +864,11 @@ extern "C" int32_t swb_set_option(swb_ctx* ctx, const char* name, int64_t value)
   }
   if (!strcmp(name, "p2_R")) {
     ctx->p2_R = (int)value;
+    return SWB_OK;
+  }
+  if (!strcmp(name, "map_tile_log2")) {
+    if (value < 8 || value > 12) return swb_fail(SWB_EINVAL, "map_tile_log2 must be in [8, 12]");
+    ctx->map_shift = (int)value;  // takes effect at the next swb_bounds_reset
     return SWB_OK;
   }
   if (!strcmp(name, "chain_chunk")) {

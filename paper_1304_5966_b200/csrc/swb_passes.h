@@ -42,6 +42,7 @@ struct PassReq {
   int32_t* bmap_out = nullptr;
   const int32_t* bmap_in = nullptr;
   int map_nr = 0, map_nc = 0, map_r0 = 0, map_rdir = 1, map_c0 = 0, map_cdir = 1;
+  int map_shift = 10;  // log2 of the tile edge
   long long bound_offset = 0;
   int4* bmap_live = nullptr;          // live-range sweep hulls per row tile (writer)
   const int4* rmap_live = nullptr;    // reader side of the same

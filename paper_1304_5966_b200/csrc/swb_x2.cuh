@@ -190,7 +190,7 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
   BoundWriter bw;  // tile bound map of this pass's H
   if (J.bmap_out) {
     const int r_hi = (R0 + 64 * R < n1 ? R0 + 64 * R : n1) - 1;
-    tile_range(J.map_r0, J.map_rdir, R0, r_hi, J.map_nr, bw.rt_lo, bw.rt_hi);
+    tile_range(J.map_r0, J.map_rdir, R0, r_hi, J.map_nr, J.map_shift, bw.rt_lo, bw.rt_hi);
   }
 
   // FINAL (last item of a pass that wants its final rows, split mode): the lane,
@@ -394,7 +394,7 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
       const int hi = s0 + 31 < n2 - 1 ? s0 + 31 : n2 - 1;
       if (lo <= hi) {
         int ta, tb;
-        tile_range(J.map_c0, J.map_cdir, lo, hi, J.map_nc, ta, tb);
+        tile_range(J.map_c0, J.map_cdir, lo, hi, J.map_nc, J.map_shift, ta, tb);
         const long long inm = (long long)mabs_w + goe;
         bw_add(J, bw, ta, tb, (inm > 0 ? inm : 0) + 95LL * P.max_sub, lane);
       }

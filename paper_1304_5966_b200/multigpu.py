@@ -547,6 +547,7 @@ class _DeviceRows:
 
 
 def map_row_tiles(slab: Slab, tile_rows: int = 1024) -> tuple[int, int]:
+    # tile_rows: 2 ** ctx.get_option("map_tile_log2") of the maps in use
     """Forward-map row tiles [lo, hi) a slab's pass writes (slabs are cut in
     multiples of 1024 rows, so neighbouring slabs never share a tile row)."""
     return slab.row0 // tile_rows, -(-slab.row1 // tile_rows)
@@ -621,8 +622,9 @@ def align_distributed(seq1, seq2, scheme, config=None, report: dict | None = Non
             if S.bounds and world > 1:
                 ptr, n, nc = ctx.bounds_device(1)
                 full = torch.as_tensor(_DeviceRows(ptr, n), device=f"cuda:{local}")
+                tile_rows = 1 << ctx.get_option("map_tile_log2")
                 for g in range(1, world):
-                    lo, hi = map_row_tiles(slabs[g])
+                    lo, hi = map_row_tiles(slabs[g], tile_rows)
                     if hi <= lo or slabs[g].rows == 0:
                         continue
                     part = full[lo * nc:hi * nc]
