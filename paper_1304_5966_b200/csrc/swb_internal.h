@@ -61,7 +61,6 @@ struct swb_ctx {
   int live_ranges = 3;  // restricted passes: bit 0 late start, bit 1 early exit
   int claim_log_on = 0; // option claim_log: record claims in a device ring (swb_debug_claims)
   int chain_chunk = 8;  // strips per CTA of chain-shaped passes (4 or 8)
-  int x2_defer = 0;     // packed kernel: deferred progress release (swb_x2.cuh)
   int min_R = 0;        // smallest rows-per-lane the shape model may pick (diagnostics)
   int wide_log2 = 28;   // passes with dynamic range >= 2^wide_log2 run on the int64 kernel
   int watchdog_ms = 0;  // > 0: report a pass launch still running after this long

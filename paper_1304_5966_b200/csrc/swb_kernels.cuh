@@ -139,8 +139,7 @@ struct PassParams {
   int32_t chunk;            // > 0: CTA claims `chunk` consecutive strips (item_map: job, first)
   int32_t big;              // substitution table mode (tab) instead of tlo/thi
   const int32_t* tab;       // 32 x 33 table, device (big schemes)
-  int32_t defer_pub;              // packed kernel: release each block's progress one block late
-  int32_t pad_pp;
+  int32_t pad_pp[2];
   unsigned long long launch_id;   // diagnostics: context launch counter at this launch
   unsigned long long* claim_log;  // diagnostics ring (claim_log in swb_kernels.cuh) or null
   unsigned long long* strip_dbg;  // per strip (item_base + s) 8 words: ranges, exit,

@@ -265,7 +265,7 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     }
   for (PassReq& r : reqs)
     r.x2 = x2_scheme && r.local && r.track == kTrackMin && !r.has_band &&
-           r.prune <= 1 &&
+           r.prune <= 1 && (!r.bmap_out || r.map_shift == kX2MapShift) &&
            // relative 16-bit frames: only the absolute H (boundary rows, running
            // best) must fit int32, which the wide limit already guarantees when
            // it is at its default
@@ -538,7 +538,6 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     if (!d_sdbg) return swb_fail(SWB_ECUDA, "out of device memory (strip diagnostics)");
     P.strip_dbg = d_sdbg;
     P.launch_id = (unsigned long long)ctx->launches;
-    P.defer_pub = ctx->x2_defer;
     if (ctx->claim_log_on) {
       if (!ctx->claim_log.p) {
         if (!swb_scratch(ctx->claim_log, 8 * (8 + 4 * 4096))) return swb_fail(SWB_ECUDA, "claim log");
@@ -813,7 +812,6 @@ extern "C" int64_t swb_get_option(swb_ctx* ctx, const char* name) {
   if (!strcmp(name, "live_big")) return ctx->live_big;
   if (!strcmp(name, "watchdog_ms")) return ctx->watchdog_ms;
   if (!strcmp(name, "wide_log2")) return ctx->wide_log2;
-  if (!strcmp(name, "x2_defer")) return ctx->x2_defer;
   if (!strcmp(name, "chain_chunk")) return ctx->chain_chunk;
   if (!strcmp(name, "map_tile_log2")) return ctx->bmap_seq1 >= 0 ? ctx->bmap_shift : ctx->map_shift;
   if (!strcmp(name, "p2_R")) return ctx->p2_R;
@@ -874,10 +872,6 @@ extern "C" int32_t swb_set_option(swb_ctx* ctx, const char* name, int64_t value)
   if (!strcmp(name, "chain_chunk")) {
     if (value != 4 && value != 8) return swb_fail(SWB_EINVAL, "chain_chunk must be 4 or 8");
     ctx->chain_chunk = (int)value;
-    return SWB_OK;
-  }
-  if (!strcmp(name, "x2_defer")) {
-    ctx->x2_defer = (int)value;
     return SWB_OK;
   }
   if (!strcmp(name, "min_R")) {

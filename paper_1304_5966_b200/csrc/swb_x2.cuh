@@ -58,6 +58,10 @@ namespace swb {
 constexpr int kX2Off = 1024;     // rel value of the floor
 constexpr int kX2Span = 26000;   // max - base kept below this
 constexpr int kX2KeyRoom = 1022; // key t field stays <= 1023
+// Tile edge of the bound maps this kernel writes: a compile-time 1024 (the
+// runtime edge of swb_kernels.cuh cost 5 % of an unrelated pass here through
+// register allocation, even unexecuted); the host keeps other edges off it.
+constexpr int kX2MapShift = 10;
 
 struct WarpSmemX2 {
   uint32_t prof[96];  // profile word of column s0 - 64 + w (0 outside [0, n2))
@@ -190,7 +194,7 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
   BoundWriter bw;  // tile bound map of this pass's H
   if (J.bmap_out) {
     const int r_hi = (R0 + 64 * R < n1 ? R0 + 64 * R : n1) - 1;
-    tile_range(J.map_r0, J.map_rdir, R0, r_hi, J.map_nr, J.map_shift, bw.rt_lo, bw.rt_hi);
+    tile_range(J.map_r0, J.map_rdir, R0, r_hi, J.map_nr, kX2MapShift, bw.rt_lo, bw.rt_hi);
   }
 
   // FINAL (last item of a pass that wants its final rows, split mode): the lane,
@@ -206,8 +210,6 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
   }
 
   int known_prog = 0, prune_seen = 0, published = 0;
-  const bool defer = P.defer_pub && !ext_out;
-  int pending_pub = 0;
   int code_next = (lane < n2) ? (int)J.cols[(long long)lane * J.cstep] : 0;
   long long pruned_blocks = 0, exec_blocks = 0, wait_cycles = 0;
   const long long t_strip0 = clock64();
@@ -394,7 +396,7 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
       const int hi = s0 + 31 < n2 - 1 ? s0 + 31 : n2 - 1;
       if (lo <= hi) {
         int ta, tb;
-        tile_range(J.map_c0, J.map_cdir, lo, hi, J.map_nc, J.map_shift, ta, tb);
+        tile_range(J.map_c0, J.map_cdir, lo, hi, J.map_nc, kX2MapShift, ta, tb);
         const long long inm = (long long)mabs_w + goe;
         bw_add(J, bw, ta, tb, (inm > 0 ? inm : 0) + 95LL * P.max_sub, lane);
       }
@@ -506,16 +508,8 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     }
     __syncwarp();
 
-    // (4) flush B's bottom row for columns [s0 - 63, s0 - 31) and publish.
-    // Deferred publication (P.defer_pub): the progress covering the PREVIOUS
-    // block is released before this block's stores, so the release's fence
-    // finds that block's stores long complete instead of stalling on the ones
-    // just issued; consumers trail by one more block.
+    // (4) flush B's bottom row for columns [s0 - 63, s0 - 31) and publish
     {
-      if (defer) {
-        if (lane == 0 && pending_pub > 0) st_release(my_progress, pending_pub);
-        __syncwarp();
-      }
       const int cf = s0 - 63 + lane;
       if (cf >= 0 && cf < n2) {
         int2 o = make_int2(-goe, SWB_NEG32);  // pruned block: the fill values
@@ -528,13 +522,13 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
       }
       if (ext_out) __threadfence_system();
       __syncwarp();
-      int pub = s0 - 31;
-      if (pub > n2) pub = n2;
-      if (defer) {
-        pending_pub = pub;
-      } else if (lane == 0 && pub > 0) {
-        if (ext_out) st_release_sys(my_progress, pub);
-        else st_release(my_progress, pub);
+      if (lane == 0) {
+        int pub = s0 - 31;
+        if (pub > n2) pub = n2;
+        if (pub > 0) {
+          if (ext_out) st_release_sys(my_progress, pub);
+          else st_release(my_progress, pub);
+        }
       }
     }
 
