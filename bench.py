@@ -240,6 +240,45 @@ def cpu_window(a, b, target_s: float = 15.0):
                       f"({dt:.1f} s, score {score})"}, w, dt
 
 
+def reference_numba_window(a, b, target_s: float = 10.0) -> dict | None:
+    """The unmodified reference itself (`wavealign`, pip-installed in
+    baseline/_ref, numba kernels, all host cores as workers) timed on a square
+    window of the same pair: informational beside the C port, which is the
+    (faster, so conservative) reference arm.  None when baseline/_ref is
+    missing."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "wavealign").is_dir():
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_swb")
+    sys.path.insert(0, str(ref))
+    try:
+        import wavealign as wa
+    except ImportError as exc:
+        return {"unavailable": f"cannot import the reference: {exc}"}
+    workers = os.cpu_count() or 1
+    alpha = wa.Alphabet.dna()
+    scheme = wa.ScoringScheme.match_mismatch(alpha, 1, -3, 5, 2)
+    sym = np.frombuffer(b"ACGT", dtype=np.uint8)
+
+    def run(w):
+        s1 = wa.Sequence.make("t", sym[a[:w]].tobytes().decode(), alpha)
+        s2 = wa.Sequence.make("q", sym[b[:w]].tobytes().decode(), alpha)
+        t0 = time.perf_counter()
+        r = wa.score_only(s1, s2, scheme, wa.AlignConfig(workers=workers))
+        return time.perf_counter() - t0, r.score
+
+    run(2000)  # numba JIT compile
+    probe = min(8000, a.size, b.size)
+    dt, _ = run(probe)
+    rate = probe * probe / max(dt, 1e-3)
+    w = int(min(a.size, b.size, max(probe, (rate * target_s) ** 0.5)))
+    dt, score = run(w)
+    return {"value": w * w / dt / 1e9, "unit": "GCUPS", "cores": workers,
+            "kind": "reference (wavealign, numba)",
+            "sample": f"score_only on the first {w} x {w} residues of the same pair "
+                      f"({dt:.1f} s, score {score}), AlignConfig(workers={workers})"}
+
+
 def align_e2e(swb, scheme, cpu_gcups, with_cpu: bool):
     """End-to-end alignment time through the public API (`align`, host
     buffers, phases 1-3), BASELINE configs C1 and C3.  C1 is also run on the
@@ -305,6 +344,12 @@ def run_reference(args, rank, world):
             secs.append(dt)
             base = cb
     value = statistics.mean(vals)
+    numba_ref = None
+    if not args.no_numba:
+        try:
+            numba_ref = reference_numba_window(a, b, target_s=min(10.0, args.cpu_seconds))
+        except Exception as exc:  # informational only: never fail the arm
+            numba_ref = {"unavailable": f"{type(exc).__name__}: {exc}"}
     line = {
         "metric": "GCUPS (score pass, full-matrix cells / time)", "value": value, "unit": "GCUPS",
         "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -315,7 +360,8 @@ def run_reference(args, rank, world):
                    "scheme": "match +1 / mismatch -3 / gap 5+2k",
                    "sample": "square window of the pair per step (see cpu_baseline.sample)"},
         "cpu_baseline": {"value": value, "unit": "GCUPS", "cores": base["cores"], "kind": "port",
-                         "cpu_model": base["cpu_model"], "sample": base["sample"]},
+                         "cpu_model": base["cpu_model"], "sample": base["sample"],
+                         "reference_numba": numba_ref},
         "e2e": {"value": value, "unit": "GCUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -464,6 +510,8 @@ def main():
     ap.add_argument("--unrelated", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-numba", action="store_true",
+                    help="reference arm: skip timing the numba reference itself (baseline/_ref)")
     ap.add_argument("--no-align", action="store_true",
                     help="skip the end-to-end alignment section (C1 vs CPU port, C3)")
     args = ap.parse_args()

@@ -10,7 +10,7 @@ ROOT = Path(__file__).resolve().parents[1]
 
 def test_reference_arm_json_line():
     out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--steps", "1",
-                          "--warmup", "0", "--cpu-seconds", "0.2", "--n", "30000"],
+                          "--warmup", "0", "--cpu-seconds", "0.2", "--n", "30000", "--no-numba"],
                          capture_output=True, text=True, check=True, cwd=ROOT, timeout=300)
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1
