@@ -9,7 +9,7 @@ from bench import synthetic_pair
 import paper_1304_5966_b200 as swb
 from paper_1304_5966_b200.engine import get_context
 
-sc = swb.ScoringScheme.match_mismatch(swb.Alphabet.dna(wildcard=False), 1, -3, 5, 2)
+sc = swb.ScoringScheme.match_mismatch(swb.Alphabet.dna(), 1, -3, 5, 2)  # the bench alphabet
 ctx = get_context(0)
 for which in sys.argv[1:]:
     if which in ("c4", "c3s"):
