@@ -177,7 +177,7 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
   // per-block key frame: V_ref per half, 1 - V_ref(rel) and the best's key
   long long vrA = 0, vrB = 0;
   uint32_t nv2 = 0u, kb2 = 0u, bk2 = 0u;
-  uint32_t bmax2 = 0u;   // optimistic blocks: packed maximum of hm over the block
+  uint32_t bmax2 = 0u;   // optimistic blocks: packed maximum of E every 4th step
   int opt_cool = 0;      // candidate blocks to track directly after a hit
   auto set_frame = [&](long long mabs_w) {
     const long long lowv = mabs_w + 95LL * P.max_sub - kX2KeyRoom;
@@ -219,7 +219,7 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
 
   auto step = [&](const int k, const int st, const bool guard, uint32_t (&Hin)[R],
                   uint32_t (&Hout)[R], auto trk_tag) {
-    constexpr int MODE = decltype(trk_tag)::value;  // 0 untracked, 1 keys, 2 column max only
+    constexpr int MODE = decltype(trk_tag)::value;  // 0 untracked, 1 keys, 2 optimistic (= 0 here)
     constexpr bool TRK = MODE == 1;
     const int colA = st - lane, colB = colA - 32;
     const int2 tp = sm->tz[tz_off + k];
@@ -242,7 +242,6 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     uint32_t fv = up_f;
     uint32_t hab = up_h;
     uint32_t cm = guard ? 0u : bk2, kp = 0u;
-    uint32_t vmx = 0u, vkp = 0u;
     uint32_t fh = 0u, ff = 0u;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -261,11 +260,6 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
         fh = hm;
         ff = fv;
       }
-      if (MODE == 2) {
-        if (r & 1) vmx = vimax3_2(vmx, vkp, hm);
-        else if (r == R - 1) vmx = vimax3_2(vmx, hm, hm);
-        vkp = hm;
-      }
       if (TRK) {
         const uint32_t t = viaddmax_relu_2(hm, nv2, NGE2);  // any c <= 0: max(hm + nv, 0)
         const uint32_t key = (uint32_t)imad((int)t, k32, (int)rk[r]);
@@ -276,7 +270,6 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     }
     out_hm = Hout[R - 1];
     out_f = fv;
-    if (MODE == 2) bmax2 = vimax3_2(bmax2, vmx, vmx);
     if (TRK) {
       bk2 = guard ? vimax3_2(bk2, cm & ~keep, 0u) : cm;
       sm->trk[k][lane] = bk2;
@@ -428,8 +421,8 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
       if (steady && track_block && opt_cool == 0) {
         // Optimistic: the block can only matter if one of its cells reaches
         // the running best (a smaller cell is never the endpoint).  Run it
-        // with a packed column max only (0.5 instead of 1.5 ALU per pair) and
-        // re-run it tracked from the saved state if the maximum reaches it.
+        // untracked with an upper bound of its maximum and re-run it tracked
+        // from the saved state if the bound reaches the best.
         uint32_t Hs[R], Es[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -437,15 +430,23 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
           Es[r] = E[r];
         }
         const uint32_t diag_s = diag, ohm_s = out_hm, of_s = out_f;
+        // E' = max(E - ge, hm) >= hm, so E after step k + 3 bounds hm of steps
+        // k .. k + 3 from above within 3 ge: one packed maximum of E every
+        // four steps bounds the block's maximum (0.125 instead of 0.5 ALU per pair)
         bmax2 = 0u;
 #pragma unroll 1
-        for (int k = 0; k < 32; k += 2) {
+        for (int k = 0; k < 32; k += 4) {
           step(k, s0 + k, false, H, H2, T2{});
           step(k + 1, s0 + k + 1, false, H2, H, T2{});
+          step(k + 2, s0 + k + 2, false, H, H2, T2{});
+          step(k + 3, s0 + k + 3, false, H2, H, T2{});
+#pragma unroll
+          for (int r = 0; r + 1 < R; r += 2) bmax2 = vimax3_2(bmax2, E[r], E[r + 1]);
+          if (R & 1) bmax2 = vimax3_2(bmax2, E[R - 1], E[R - 1]);
         }
         const int mrel2 = __reduce_max_sync(0xffffffffu, lo16(bmax2) > hi16(bmax2) ? lo16(bmax2)
                                                                                     : hi16(bmax2));
-        if ((long long)mrel2 + base - kX2Off + goe >= (long long)prune_seen) {
+        if ((long long)mrel2 + 3LL * ge + base - kX2Off + goe >= (long long)prune_seen) {
 #pragma unroll
           for (int r = 0; r < R; ++r) {
             H[r] = Hs[r];
