@@ -865,7 +865,10 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
             if (ay > 0) ahi_p = ay - 1;
           }
         } else if (known_prog < need) {
-          if ((ext_in ? ld_relaxed_sys(up_progress) : ld_relaxed(up_progress)) < need) {
+          // one acquiring load when the producer is already ahead; poll
+          // relaxed only when it is not
+          known_prog = ext_in ? ld_acquire_sys(up_progress) : ld_acquire(up_progress);
+          if (known_prog < need) {
             const long long tw = clock64();
             unsigned long long a0, a1;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a0));
@@ -873,8 +876,8 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a1));
             gw += a1 - a0;
             wait_cycles += clock64() - tw;
+            known_prog = ext_in ? ld_acquire_sys(up_progress) : ld_acquire(up_progress);
           }
-          known_prog = ext_in ? ld_acquire_sys(up_progress) : ld_acquire(up_progress);
           if (dyn && ahi_p == 0x7fffffff) {
             const int ay = ld_relaxed(&J.alive[SWB_IX(s - 1, J.nstrips)].y);
             if (ay > 0) ahi_p = ay - 1;

@@ -307,7 +307,10 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
       if (has_top && s0 < n2) {
         const int need = (s0 + 32 < n2) ? s0 + 32 : n2;
         if (known_prog < need) {
-          if ((ext_in ? ld_relaxed_sys(up_progress) : ld_relaxed(up_progress)) < need) {
+          // one acquiring load when the producer is already ahead (the common
+          // case off the chain); poll relaxed only when it is not
+          known_prog = ext_in ? ld_acquire_sys(up_progress) : ld_acquire(up_progress);
+          if (known_prog < need) {
             const long long tw = clock64();
             unsigned long long a0, a1;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a0));
@@ -315,8 +318,8 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a1));
             gw += a1 - a0;
             wait_cycles += clock64() - tw;
+            known_prog = ext_in ? ld_acquire_sys(up_progress) : ld_acquire(up_progress);
           }
-          known_prog = ext_in ? ld_acquire_sys(up_progress) : ld_acquire(up_progress);
         }
       }
       if (has_top && c < n2) {
