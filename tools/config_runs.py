@@ -12,9 +12,11 @@ from paper_1304_5966_b200.engine import get_context
 sc = swb.ScoringScheme.match_mismatch(swb.Alphabet.dna(), 1, -3, 5, 2)  # the bench alphabet
 ctx = get_context(0)
 for which in sys.argv[1:]:
-    if which in ("c4", "c3s"):
+    if which in ("c4", "c3s", "c5s"):
         if which == "c4":
             a, b = synthetic_pair(10_000_000, seed=1004, homologous=False)
+        elif which == "c5s":
+            a, b = synthetic_pair(32_000_000, seed=1005)
         else:
             a, b = synthetic_pair(5_000_000, seed=1003)
         s1 = swb.Sequence.from_codes("a", a, sc.alphabet); s2 = swb.Sequence.from_codes("b", b, sc.alphabet)
@@ -22,8 +24,10 @@ for which in sys.argv[1:]:
         t0 = time.perf_counter()
         r = swb.score_only(s1, s2, sc, report=rep)
         dt = time.perf_counter() - t0
-        print(json.dumps({"config": "C4 10 Mbp x 10 Mbp unrelated (seed 1004), score_only" if which == "c4"
-                          else "C3 5 Mbp homologous (seed 1003), score_only", "n1": int(a.size),
+        name = {"c4": "C4 10 Mbp x 10 Mbp unrelated (seed 1004), score_only",
+                "c3s": "C3 5 Mbp homologous (seed 1003), score_only",
+                "c5s": "C5 32 Mbp homologous (seed 1005), score_only"}[which]
+        print(json.dumps({"config": name, "n1": int(a.size),
                           "n2": int(b.size), "score": r.score, "end": list(r.end), "wall_s": round(dt, 3),
                           "gcups_e2e": round(a.size * b.size / dt / 1e9, 1),
                           **{k: v for k, v in rep.items() if isinstance(v, (int, float, str))}}), flush=True)
