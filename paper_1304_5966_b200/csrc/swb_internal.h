@@ -65,6 +65,8 @@ struct swb_ctx {
   int wide_log2 = 28;   // passes with dynamic range >= 2^wide_log2 run on the int64 kernel
   int watchdog_ms = 0;  // > 0: report a pass launch still running after this long
   int live_big = 3;     // live_ranges bits kept for shared-table (large alphabet) passes
+  int x2_blk = 0;       // packed kernel steps per block: 0 auto (rounds), 32, 64
+  int last_x2_blk = 0;  // block length of the last packed launch (diagnostics)
   int p2_R = 8;         // rows per lane of bound-pruned restricted passes (phase 2)
   int mm_R = 8;         // rows per lane of range-limited Myers-Miller passes
   int mm_static = 1;    // static strip ranges for Myers-Miller halves

@@ -34,8 +34,13 @@ int dispatch_other_track(swb_ctx* ctx, int R, const PassParams* P, long long ite
                          int ctas_per_sm, int* occ_out);
 int dispatch_big(swb_ctx* ctx, int R, const PassParams* P, long long items, bool local, int track,
                  int ctas_per_sm, int* occ_out);
+// blk: steps per block of the packed kernel, 32 or 64 (swb_x2.cuh)
 int dispatch_x2(swb_ctx* ctx, int R, const PassParams* P, long long items, int ctas_per_sm,
-                int* occ_out, bool wild = false, bool final_rows = false);
+                int* occ_out, bool wild = false, bool final_rows = false, int blk = 32);
+int dispatch_x2_b32(swb_ctx* ctx, int R, const PassParams* P, long long items, int ctas_per_sm,
+                    int* occ_out, bool wild, bool final_rows);
+int dispatch_x2_b64(swb_ctx* ctx, int R, const PassParams* P, long long items, int ctas_per_sm,
+                    int* occ_out, bool wild, bool final_rows);
 
 // checked builds: each translation unit reports (and clears) its own record
 int chk_take_local(long long* out);
@@ -67,11 +72,15 @@ int kernel_occupancy(int* per_sm) {
       per_sm, pass_kernel<R, LOCAL, TRACK, BIG>, 128, 0);
 }
 
+// warp_smem > 0: the kernel takes warp_smem bytes of dynamic shared memory per
+// warp plus 64 (the packed kernel, x2_smem_bytes); 0: static shared memory only
 template <typename K>
-int launch_any(swb_ctx* ctx, K kern, const PassParams& Pin, long long items, int ctas_per_sm) {
+int launch_any(swb_ctx* ctx, K kern, const PassParams& Pin, long long items, int ctas_per_sm,
+               size_t warp_smem = 0) {
   PassParams P = Pin;
+  auto dyn = [&](int threads) -> size_t { return warp_smem ? (threads / 32) * warp_smem + 64 : 0; };
   int per_sm = 0;
-  SWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, 0));
+  SWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, dyn(128)));
   if (per_sm < 1) return swb_fail(SWB_ECUDA, "pass kernel does not fit on an SM");
   if (ctas_per_sm > 0 && per_sm > ctas_per_sm) per_sm = ctas_per_sm;
   if (P.chunk > 0) {
@@ -79,11 +88,11 @@ int launch_any(swb_ctx* ctx, K kern, const PassParams& Pin, long long items, int
     const int grid = (int)std::min(cap, std::max((long long)P.total_items, 1LL));
     int per = per_sm;
     if (P.chunk > 4) {  // 8-warp chunks: occupancy of the wider CTA
-      SWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 32 * P.chunk, 0));
+      SWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 32 * P.chunk, dyn(32 * P.chunk)));
       if (per < 1) return swb_fail(SWB_ECUDA, "chunk CTA does not fit on an SM");
     }
     const int grid2 = (int)std::min((long long)per * ctx->sms, std::max((long long)P.total_items, 1LL));
-    kern<<<P.chunk > 4 ? grid2 : grid, 32 * P.chunk, 0, ctx->stream>>>(P);
+    kern<<<P.chunk > 4 ? grid2 : grid, 32 * P.chunk, dyn(32 * P.chunk), ctx->stream>>>(P);
     ctx->launches++;
     SWB_CUDA(cudaGetLastError());
     return SWB_OK;
@@ -93,14 +102,14 @@ int launch_any(swb_ctx* ctx, K kern, const PassParams& Pin, long long items, int
     // one CTA per SM, per_sm warps per sub-partition, adjacent strips paired
     const int threads = 128 * per_sm;
     int fit = 0;
-    SWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, kern, threads, 0));
+    SWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, kern, threads, dyn(threads)));
     if (fit >= 1) {
       // adjacent strips of one chain share a sub-partition: job-major order
       P.item_map = nullptr;
       P.group = 4 * per_sm;
       P.mirror = (per_sm == 2 && items <= 8LL * ctx->sms && ctx->proto != 8) ? 1 : 0;
       // dynamic shared memory pins the layout to exactly one CTA per SM
-      const int pin = 120 * 1024;
+      const int pin = (int)std::max<size_t>(120 * 1024, dyn(threads));
       SWB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pin));
       kern<<<ctx->sms, threads, pin, ctx->stream>>>(P);
       ctx->launches++;
@@ -113,7 +122,7 @@ int launch_any(swb_ctx* ctx, K kern, const PassParams& Pin, long long items, int
   long long cap = (long long)per_sm * ctx->sms;
   long long need = (items + 3) / 4;
   int grid = (int)std::min(cap, std::max(need, 1LL));
-  kern<<<grid, 128, 0, ctx->stream>>>(P);
+  kern<<<grid, 128, dyn(128), ctx->stream>>>(P);
   ctx->launches++;
   SWB_CUDA(cudaGetLastError());
   return SWB_OK;

@@ -241,10 +241,11 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
                       sc.goe >= (lim >> 2) - 64);
   }
   // packed 16x2 fast path eligibility (swb_x2.cuh header)
-  // 95 max_sub <= 1021: 16-bit endpoint keys (swb_x2.cuh).  Window bound:
-  // neighbouring cells differ by at most go + ge + max_sub, so every value of a
-  // warp's window (<= 1024 rows + 96 columns, plus 32 columns of growth) lies
-  // within kX2Span of the window maximum and the relative frame never clamps one.
+  // W max_sub <= 1021 (W = BLK + 63 columns of a block's window): 16-bit
+  // endpoint keys (swb_x2.cuh).  Window bound: neighbouring cells differ by at
+  // most go + ge + max_sub, so every value of a warp's window (<= 1024 rows + W
+  // columns, plus BLK columns of growth) lies within kX2Span of the window
+  // maximum and the relative frame never clamps one (x2_frame_ok).
   const long long ms = std::max(sc.max_sub, 0);
   // Five codes are allowed when code 4 scores the same against every column
   // (the default DNA alphabet's 'N' wildcard): its rows take a constant added
@@ -257,7 +258,9 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     if (wild_const > 127) wild_const = -1;
   }
   bool x2_scheme = (sc.k <= 4 || wild_const >= 0) && !sc.big && ctx->x2_enabled &&
-                   95 * ms <= 1021 && 1120LL * (sc.goe + ms) + 32LL * ms + sc.goe <= 25000;
+                   x2_frame_ok(32, sc.goe, ms);
+  // 64-step blocks need the wider window's key room and frame (swb_x2.cuh)
+  const bool x2_blk64_ok = x2_frame_ok(64, sc.goe, ms);
   for (int b = 0; b < sc.k && x2_scheme; ++b)
     for (int a = 0; a < 4 && a < sc.k; ++a) {
       const int v = (int)(int8_t)((sc.tlo[b] >> (8 * a)) & 0xff);
@@ -564,7 +567,14 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     P.wild_const = wild_const;
     bool any_final_x2 = false;
     for (size_t t = g0; t < g1; ++t) any_final_x2 |= head.x2 && reqs[order[t]].want_final;
-    rc = head.x2  ? dispatch_x2(ctx, R, &P, item, ctas, nullptr, head.x2_wild, any_final_x2)
+    // packed kernel block length: 64 steps (half the handoffs, releases and
+    // re-bases per column) for passes of more than one round of items; 32 for
+    // single-round passes, where the longer handoff lag and the longer
+    // optimistic re-runs cost more than they save
+    const int x2_blk = (ctx->x2_blk == 64 || (ctx->x2_blk == 0 && item > (long long)ctx->sms * 8))
+                           && x2_blk64_ok ? 64 : 32;
+    if (head.x2) ctx->last_x2_blk = x2_blk;
+    rc = head.x2  ? dispatch_x2(ctx, R, &P, item, ctas, nullptr, head.x2_wild, any_final_x2, x2_blk)
          : sc.big ? dispatch_big(ctx, R, &P, item, head.local, head.track, ctas, nullptr)
                   : dispatch(ctx, R, &P, item, head.local, head.track, ctas, nullptr);
     if (rc) return rc;
@@ -679,7 +689,9 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
       r.blocks_pruned = (long long)h_cnt[5 * t + 2];
       ctx->dbg_wait_cycles += (long long)h_cnt[5 * t + 3];
       ctx->dbg_strip_cycles += (long long)h_cnt[5 * t + 4];
-      r.blocks_total = (long long)r.nstrips * ((r.n2 + 31) / 32);
+      // packed kernel: every block of every item is executed or pruned
+      r.blocks_total = r.x2 ? r.blocks_exec + r.blocks_pruned
+                            : (long long)r.nstrips * ((r.n2 + 31) / 32);
     }
     g0 = g1;
   }
@@ -800,6 +812,8 @@ extern "C" int64_t swb_get_option(swb_ctx* ctx, const char* name) {
   if (!ctx || !name) return -1;
   if (!strcmp(name, "max_ctas_per_sm")) return ctx->max_ctas_per_sm;
   if (!strcmp(name, "x2_R")) return ctx->x2_R;
+  if (!strcmp(name, "x2_blk")) return ctx->x2_blk;
+  if (!strcmp(name, "last_x2_blk")) return ctx->last_x2_blk;
   if (!strcmp(name, "x2")) return ctx->x2_enabled;
   if (!strcmp(name, "job_major")) return ctx->job_major;
   if (!strcmp(name, "bound_maps")) return ctx->bmaps_on;
@@ -826,6 +840,11 @@ extern "C" int32_t swb_set_option(swb_ctx* ctx, const char* name, int64_t value)
   if (!ctx || !name) return swb_fail(SWB_EINVAL, "bad arguments");
   if (!strcmp(name, "max_ctas_per_sm")) {
     ctx->max_ctas_per_sm = (int)value;
+    return SWB_OK;
+  }
+  if (!strcmp(name, "x2_blk")) {
+    if (value != 0 && value != 32 && value != 64) return swb_fail(SWB_EINVAL, "x2_blk must be 0, 32 or 64");
+    ctx->x2_blk = (int)value;  // 0: by rounds of items
     return SWB_OK;
   }
   if (!strcmp(name, "x2_R")) {

@@ -22,23 +22,25 @@
 // 26000 below the warp's maximum, which no true value in the warp's window can:
 // by induction over rows and columns, neighbouring cells of H (and E, F against
 // their H) differ by at most max_sub + go + ge, the window spans at most 1024
-// rows + 96 columns, and the host only selects this kernel when
-// 1120 (go + ge + max_sub) + 32 max_sub + go + ge <= 25000.  So no value is ever
-// clamped by the frame and every value is exact.  The base is
-// re-chosen every 32 steps from the warp maximum and the incoming top row.
+// rows + W columns (W = BLK + 63, BLK = 64 steps per block), and the host only
+// selects this kernel when (1025 + W)(go + ge + max_sub) + BLK max_sub + go + ge
+// <= 25000.  So no value is ever clamped by the frame and every value is exact
+// (DESIGN.md §3.5).  The base is re-chosen every block from the warp maximum
+// and the incoming top row.
 //
 // Endpoint tracking (reference TRACK_MIN: largest score, then smallest row,
 // then smallest column) uses packed 16-bit keys relative to a per-block
-// reference V_ref = max(V, M + 95 max_sub - 1022) of each lane half, V its
+// reference V_ref = max(V, M + W max_sub - 1022) of each lane half, V its
 // running best and M the warp maximum at the block start:
 //   key = 32 * max(hm - V_ref + 1, 0) + (31 - r).
-// No cell of the 95-column block exceeds M + 95 max_sub, so keys stay below
+// No cell of the W-column block exceeds M + W max_sub, so keys stay below
 // 32768 and are exact; cells below V_ref are below M, hence strictly below the
 // final best, and cannot be the endpoint.  Each step folds its keys into a
-// running maximum that is also stored to shared memory; at the block end a
-// half whose maximum beats its best's key (32 + rank, or 31 when V_ref > V)
-// binary-searches the stored maxima for the first step that reached it.
-// Requires 95 max_sub <= 1021.
+// running maximum that is also stored to shared memory; at the end of each
+// 32-step half of a block a lane half whose maximum beats its best's key
+// (32 + rank, or 31 when V_ref > V) binary-searches the stored maxima for the
+// first step that reached it, and the keys are re-framed on the new best.
+// Requires W max_sub <= 1021.
 //
 // The producer's row enters through lane 0 as IMAD(shfl(x), 65536, top): the
 // shuffle from lane 31 moves A's bottom into B's half while the top value
@@ -62,13 +64,27 @@ constexpr int kX2KeyRoom = 1022; // key t field stays <= 1023
 // runtime edge of swb_kernels.cuh cost 5 % of an unrelated pass here through
 // register allocation, even unexecuted); the host keeps other edges off it.
 constexpr int kX2MapShift = 10;
-
+// Steps per block BLK (one producer handoff, one release, one re-base per
+// block): 32, or 64 for passes of several rounds of items (the host's choice,
+// swb_pass.cu); a 64-step block tracks in two 32-step halves (keys resolved
+// per half).  A block's skewed window spans BLK + 63 columns.
+template <int BLK>
 struct WarpSmemX2 {
-  uint32_t prof[96];  // profile word of column s0 - 64 + w (0 outside [0, n2))
-  int2 tz[64];        // [0, 32): rel (h, f) of the producer's row at column s0 + k; [32, 64): 0
-  uint2 out[32];      // raw packed (hm, F) of lane 31 at step k (B's bottom row)
-  uint32_t trk[32][32];  // [k][lane]: running packed key maximum after step k
+  static_assert(BLK == 32 || BLK == 64, "packed block length");
+  uint32_t prof[BLK + 64];  // profile word of column s0 - 64 + w (0 outside [0, n2))
+  int2 tz[2 * BLK];         // [0, BLK): rel (h, f) of the producer's row at s0 + k; then 0
+  uint2 out[BLK];           // raw packed (hm, F) of lane 31 at step k (B's bottom row)
+  uint32_t trk[32][32];     // [k][lane]: running packed key maximum after step k (per half)
 };
+// per CTA of `warps` warps: the warps' areas, then the 8 profile words
+template <int BLK>
+__host__ __device__ constexpr size_t x2_smem_bytes(int warps) {
+  return (size_t)warps * sizeof(WarpSmemX2<BLK>) + 64;
+}
+// host eligibility of a scheme for block length blk (header: keys and frame)
+__host__ __device__ constexpr bool x2_frame_ok(int blk, long long goe, long long ms) {
+  return (blk + 63) * ms <= 1021 && (1025LL + blk + 63) * (goe + ms) + blk * ms + goe <= 25000;
+}
 
 __device__ __forceinline__ uint32_t vimax3_2(uint32_t a, uint32_t b, uint32_t c) {
   return (uint32_t)__vimax3_s16x2((int)a, (int)b, (int)c);
@@ -88,9 +104,11 @@ __device__ __forceinline__ int clamp_rel(long long v) {
   return v < 0 ? 0 : (v > 32767 ? 32767 : (int)v);
 }
 
-template <int R, bool WILD, bool FINAL>
+template <int R, bool WILD, bool FINAL, int BLK>
 __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& Jg, int s,
-                                          WarpSmemX2* sm, const uint32_t* __restrict__ tw_s) {
+                                          WarpSmemX2<BLK>* sm, const uint32_t* __restrict__ tw_s) {
+  constexpr int kX2Blk = BLK;
+  constexpr int kX2Win = BLK + 63;  // columns a block's skewed window spans
   static_assert(R <= 32, "rank field is 5 bits");
   // by-value copy of the job descriptor: its fields live in registers in the
   // hot loop (a reference instead: 192 registers, but C2 246 -> 263 ms); the
@@ -141,8 +159,8 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
   // Every profile word an inactive half may read must be a valid one: a byte
   // >= 128 would be sign-replicated by PRMT and its carry in the packed IMAD
   // add would reach the other half.
-  for (int q = lane; q < 96; q += 32) sm->prof[q] = 0u;
-  sm->tz[32 + lane] = make_int2(0, 0);
+  for (int q = lane; q < kX2Blk + 64; q += 32) sm->prof[q] = 0u;
+  for (int q = lane; q < kX2Blk; q += 32) sm->tz[kX2Blk + q] = make_int2(0, 0);
   __syncwarp();
 
   const uint32_t FLOOR2 = pack2(kX2Off, kX2Off);
@@ -153,7 +171,7 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
   const int k32 = P.key_mul;
   const int up_mul = lane == 0 ? 65536 : 1;
   const int src_lane = (lane + 31) & 31;
-  const int tz_off = lane == 0 ? 0 : 32;
+  const int tz_off = lane == 0 ? 0 : kX2Blk;
   uint32_t rk[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) rk[r] = (uint32_t)(31 - r) * 0x10001u;
@@ -180,7 +198,7 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
   uint32_t bmax2 = 0u;   // optimistic blocks: packed maximum of E every 4th step
   int opt_cool = 0;      // candidate blocks to track directly after a hit
   auto set_frame = [&](long long mabs_w) {
-    const long long lowv = mabs_w + 95LL * P.max_sub - kX2KeyRoom;
+    const long long lowv = mabs_w + (long long)kX2Win * P.max_sub - kX2KeyRoom;
     vrA = vA > lowv ? vA : lowv;
     vrB = vB > lowv ? vB : lowv;
     long long ra = vrA - base + kX2Off, rb = vrB - base + kX2Off;
@@ -210,7 +228,11 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
   }
 
   int known_prog = 0, prune_seen = 0, published = 0;
-  int code_next = (lane < n2) ? (int)J.cols[(long long)lane * J.cstep] : 0;
+  constexpr int NH = kX2Blk / 32;  // 32-column slices per block
+  int code_next[NH];
+#pragma unroll
+  for (int h = 0; h < NH; ++h)
+    code_next[h] = (32 * h + lane < n2) ? (int)J.cols[(long long)(32 * h + lane) * J.cstep] : 0;
   long long pruned_blocks = 0, exec_blocks = 0, wait_cycles = 0;
   const long long t_strip0 = clock64();
   unsigned long long g0, gw = 0, g_diag = 0;
@@ -233,7 +255,7 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     if (guard && !actA && !actB) {
 #pragma unroll
       for (int r = 0; r < R; ++r) Hout[r] = Hin[r];
-      if (TRK) sm->trk[k][lane] = bk2;
+      if (TRK) sm->trk[k & 31][lane] = bk2;
       return;
     }
     const uint32_t keep = guard ? ((actA ? 0u : 0xffffu) | (actB ? 0u : 0xffff0000u)) : 0u;
@@ -272,7 +294,7 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     out_f = fv;
     if (TRK) {
       bk2 = guard ? vimax3_2(bk2, cm & ~keep, 0u) : cm;
-      sm->trk[k][lane] = bk2;
+      sm->trk[k & 31][lane] = bk2;
     }
     if (lane == 31 && actB) sm->out[k] = make_uint2(out_hm, out_f);
     if (FINAL && lane == lstar) {
@@ -285,11 +307,15 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     }
   };
 
-  for (int s0 = 0; s0 < s_end; s0 += 32) {
-    // (1) wait for and read the producer's bottom row for [s0, s0+32); shift
+  for (int s0 = 0; s0 < s_end; s0 += kX2Blk) {
+    // (1) wait for and read the producer's bottom row for [s0, s0 + BLK); shift
     //     the profile window and stage the new columns' words
-    const int c = s0 + lane;
-    int top_h = -goe, top_f = SWB_NEG32;  // local top border: H = 0, F = -inf
+    int top_h[NH], top_f[NH];
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+      top_h[h] = -goe;  // local top border: H = 0, F = -inf
+      top_f[h] = SWB_NEG32;
+    }
     // The running best also decides tracking, so it is kept with pruning off.
     // It steers skip / tracking around the shuffling steps, so it must be the
     // same in every lane (a lane that skipped while the others ran would pair
@@ -299,13 +325,15 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     __syncwarp();
     prune_seen = load_best(J);
     {
-      const int code = code_next;
-      {
-        const int cn = c + 32;
-        code_next = (cn < n2) ? (int)J.cols[(long long)cn * J.cstep] : 0;
+      int code[NH];
+#pragma unroll
+      for (int h = 0; h < NH; ++h) {
+        code[h] = code_next[h];
+        const int cn = s0 + kX2Blk + 32 * h + lane;
+        code_next[h] = (cn < n2) ? (int)J.cols[(long long)cn * J.cstep] : 0;
       }
       if (has_top && s0 < n2) {
-        const int need = (s0 + 32 < n2) ? s0 + 32 : n2;
+        const int need = (s0 + kX2Blk < n2) ? s0 + kX2Blk : n2;
         if (known_prog < need) {
           // one acquiring load when the producer is already ahead (the common
           // case off the chain); poll relaxed only when it is not
@@ -322,16 +350,23 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
           }
         }
       }
-      if (has_top && c < n2) {
-        const int2 v = __ldcg(inbuf + c);
-        top_h = v.x;
-        top_f = v.y;
+#pragma unroll
+      for (int h = 0; h < NH; ++h) {
+        const int c = s0 + 32 * h + lane;
+        if (has_top && c < n2) {
+          const int2 v = __ldcg(inbuf + c);
+          top_h[h] = v.x;
+          top_f[h] = v.y;
+        }
       }
-      const uint32_t p1 = sm->prof[32 + lane], p2 = sm->prof[64 + lane];
+      // keep the window's last 64 columns, then the block's new ones
+      const uint32_t p1 = sm->prof[kX2Blk + lane], p2 = sm->prof[kX2Blk + 32 + lane];
       __syncwarp();
       sm->prof[lane] = p1;
       sm->prof[32 + lane] = p2;
-      sm->prof[64 + lane] = c < n2 ? tw_s[code] : 0u;
+#pragma unroll
+      for (int h = 0; h < NH; ++h)
+        sm->prof[64 + 32 * h + lane] = s0 + 32 * h + lane < n2 ? tw_s[code[h]] : 0u;
     }
 
     // (1b) re-base: warp maximum over the state and the incoming top row
@@ -342,7 +377,9 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     }
     mrel = __vimax3_s32(mrel, lo16(out_hm), hi16(out_hm));
     long long mabs = (long long)mrel + base - kX2Off;  // hm (H - go - ge), absolute
-    if (c < n2 && (long long)top_h > mabs) mabs = top_h;
+#pragma unroll
+    for (int h = 0; h < NH; ++h)
+      if (s0 + 32 * h + lane < n2 && (long long)top_h[h] > mabs) mabs = top_h[h];
     const int mabs_w = __reduce_max_sync(0xffffffffu, (int)(mabs > INT32_MAX ? INT32_MAX : mabs));
     {
       long long nb = (long long)mabs_w + goe - kX2Span;
@@ -367,18 +404,20 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
       }
     }
     // the producer's row in this block's frame (lane 0 injects it at step k)
-    sm->tz[lane] = make_int2(clamp_rel((long long)top_h - base + kX2Off),
-                             clamp_rel((long long)top_f - base + kX2Off));
+#pragma unroll
+    for (int h = 0; h < NH; ++h)
+      sm->tz[32 * h + lane] = make_int2(clamp_rel((long long)top_h[h] - base + kX2Off),
+                                        clamp_rel((long long)top_f[h] - base + kX2Off));
     __syncwarp();
-    const bool steady = (s0 >= 63) && (s0 + 32 <= n2);
-    if (P.proto == 10 && g_diag == 0 && s0 + 32 > R0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_diag));
+    const bool steady = (s0 >= 63) && (s0 + kX2Blk <= n2);
+    if (P.proto == 10 && g_diag == 0 && s0 + kX2Blk > R0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_diag));
 
-    // (2) pruning / tracking decision on the 95-column skewed block
+    // (2) pruning / tracking decision on the block's skewed window
     bool skip = false, track_block = true;
     if (steady) {
       const long long inm = (long long)mabs_w + goe;
       const long long ms = P.max_sub;
-      track_block = (inm > 0 ? inm : 0) + 95LL * ms >= (long long)prune_seen;
+      track_block = (inm > 0 ? inm : 0) + (long long)kX2Win * ms >= (long long)prune_seen;
       if (J.prune == 1) {
         const int rem_r = n1 - R0 + J.rows_after;
         const int rem_c = n2 - (s0 - 63);
@@ -389,12 +428,12 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
 
     if (J.bmap_out) {
       const int lo = s0 - 63 > 0 ? s0 - 63 : 0;
-      const int hi = s0 + 31 < n2 - 1 ? s0 + 31 : n2 - 1;
+      const int hi = s0 + kX2Blk - 1 < n2 - 1 ? s0 + kX2Blk - 1 : n2 - 1;
       if (lo <= hi) {
         int ta, tb;
         tile_range(J.map_c0, J.map_cdir, lo, hi, J.map_nc, kX2MapShift, ta, tb);
         const long long inm = (long long)mabs_w + goe;
-        bw_add(J, bw, ta, tb, (inm > 0 ? inm : 0) + 95LL * P.max_sub, lane);
+        bw_add(J, bw, ta, tb, (inm > 0 ? inm : 0) + (long long)kX2Win * P.max_sub, lane);
       }
     }
 
@@ -410,7 +449,7 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
       }
       // lane 0's next diagonal is the real top input of the block's last column
       diag = fill;
-      if (lane == 0) diag = pack2(sm->tz[31].x, hf);
+      if (lane == 0) diag = pack2(sm->tz[kX2Blk - 1].x, hf);
       out_hm = fill;
       out_f = 0u;
     } else {
@@ -438,7 +477,7 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
         // four steps bounds the block's maximum (0.125 instead of 0.5 ALU per pair)
         bmax2 = 0u;
 #pragma unroll 1
-        for (int k = 0; k < 32; k += 4) {
+        for (int k = 0; k < kX2Blk; k += 4) {
           step(k, s0 + k, false, H, H2, T2{});
           step(k + 1, s0 + k + 1, false, H2, H, T2{});
           step(k + 2, s0 + k + 2, false, H, H2, T2{});
@@ -464,70 +503,89 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
           tracked_run = false;
         }
       }
+      // a strictly better cell in at least one lane half: first step of the
+      // 32-step half [h0, h0 + 32) reaching it
+      bool found = false;
+      auto resolve_half = [&](int h0) {
+        __syncwarp();
+        found |= !__all_sync(0xffffffffu, bk2 == kb2);
+        if (bk2 != kb2) {
+          auto resolve = [&](bool hiHalf, int key, int colbase, int& v, int& rk_, int& bj,
+                             long long vref) {
+            int lo = 0;
+#pragma unroll
+            for (int stp = 16; stp > 0; stp >>= 1) {
+              const uint32_t w = sm->trk[lo + stp - 1][lane];
+              if ((hiHalf ? hi16(w) : lo16(w)) < key) lo += stp;
+            }
+            v = (int)(vref + (key >> 5) - 1);
+            rk_ = key & 31;
+            bj = colbase + lo;
+          };
+          const int ka = lo16(bk2), kbh = hi16(bk2);
+          if (ka > lo16(kb2)) resolve(false, ka, s0 + h0 - lane, vA, rkA, bjA, vrA);
+          if (kbh > hi16(kb2)) resolve(true, kbh, s0 + h0 - lane - 32, vB, rkB, bjB, vrB);
+        }
+        __syncwarp();
+        if (h0 + 32 < kX2Blk) set_frame(mabs_w);  // keys of the next half against the new best
+      };
       if (!tracked_run) {
       } else if (steady && !track_block) {
 #pragma unroll 1
-        for (int k = 0; k < 32; k += 2) {
+        for (int k = 0; k < kX2Blk; k += 2) {
           step(k, s0 + k, false, H, H2, T0{});
           step(k + 1, s0 + k + 1, false, H2, H, T0{});
         }
       } else if (steady) {
 #pragma unroll 1
-        for (int k = 0; k < 32; k += 2) {
-          step(k, s0 + k, false, H, H2, T1{});
-          step(k + 1, s0 + k + 1, false, H2, H, T1{});
+        for (int h0 = 0; h0 < kX2Blk; h0 += 32) {
+#pragma unroll 1
+          for (int k = h0; k < h0 + 32; k += 2) {
+            step(k, s0 + k, false, H, H2, T1{});
+            step(k + 1, s0 + k + 1, false, H2, H, T1{});
+          }
+          resolve_half(h0);
         }
       } else {
 #pragma unroll 1
-        for (int k = 0; k < 32; k += 2) {
-          step(k, s0 + k, true, H, H2, T1{});
-          step(k + 1, s0 + k + 1, true, H2, H, T1{});
+        for (int h0 = 0; h0 < kX2Blk; h0 += 32) {
+#pragma unroll 1
+          for (int k = h0; k < h0 + 32; k += 2) {
+            step(k, s0 + k, true, H, H2, T1{});
+            step(k + 1, s0 + k + 1, true, H2, H, T1{});
+          }
+          resolve_half(h0);
         }
       }
       __syncwarp();
       // a tracked block that found nothing new lets the next candidate try
       // the optimistic run again
       if (steady && track_block && tracked_run) {
-        if (!__all_sync(0xffffffffu, bk2 == kb2)) opt_cool = 4;
+        if (found) opt_cool = 4;
         else if (opt_cool > 0) --opt_cool;
-      }
-      if (trk_on && tracked_run && bk2 != kb2) {
-        // a strictly better cell in at least one half: first step reaching it
-        auto resolve = [&](bool hiHalf, int key, int colbase, int& v, int& rk_, int& bj,
-                           long long vref) {
-          int lo = 0;
-#pragma unroll
-          for (int stp = 16; stp > 0; stp >>= 1) {
-            const uint32_t w = sm->trk[lo + stp - 1][lane];
-            if ((hiHalf ? hi16(w) : lo16(w)) < key) lo += stp;
-          }
-          v = (int)(vref + (key >> 5) - 1);
-          rk_ = key & 31;
-          bj = colbase + lo;
-        };
-        const int ka = lo16(bk2), kbh = hi16(bk2);
-        if (ka > lo16(kb2)) resolve(false, ka, s0 - lane, vA, rkA, bjA, vrA);
-        if (kbh > hi16(kb2)) resolve(true, kbh, s0 - lane - 32, vB, rkB, bjB, vrB);
       }
     }
     __syncwarp();
 
-    // (4) flush B's bottom row for columns [s0 - 63, s0 - 31) and publish
+    // (4) flush B's bottom row for columns [s0 - 63, s0 - 63 + BLK) and publish
     {
-      const int cf = s0 - 63 + lane;
-      if (cf >= 0 && cf < n2) {
-        int2 o = make_int2(-goe, SWB_NEG32);  // pruned block: the fill values
-        if (!skip) {
-          const uint2 raw = sm->out[lane];
-          const int off = base - kX2Off;
-          o = make_int2(hi16(raw.x) + off, hi16(raw.y) + off);
+#pragma unroll
+      for (int h = 0; h < NH; ++h) {
+        const int cf = s0 - 63 + 32 * h + lane;
+        if (cf >= 0 && cf < n2) {
+          int2 o = make_int2(-goe, SWB_NEG32);  // pruned block: the fill values
+          if (!skip) {
+            const uint2 raw = sm->out[32 * h + lane];
+            const int off = base - kX2Off;
+            o = make_int2(hi16(raw.x) + off, hi16(raw.y) + off);
+          }
+          __stcg(outbuf + cf, o);
         }
-        __stcg(outbuf + cf, o);
       }
       if (ext_out) __threadfence_system();
       __syncwarp();
       if (lane == 0) {
-        int pub = s0 - 31;
+        int pub = s0 - 63 + kX2Blk;
         if (pub > n2) pub = n2;
         if (pub > 0) {
           if (ext_out) st_release_sys(my_progress, pub);
@@ -588,7 +646,7 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     J.strip_res[s] = make_int4(b, ii, jj, ii >= 0 ? 1 : 0);
     int rows_here = n1 - R0;
     if (rows_here > 64 * R) rows_here = 64 * R;
-    const long long cells = (long long)n2 * rows_here - pruned_blocks * 32LL * rows_here;
+    const long long cells = (long long)n2 * rows_here - pruned_blocks * (long long)kX2Blk * rows_here;
     atomicAdd(&J.counters[0], (unsigned long long)(cells > 0 ? cells : 0));
     atomicAdd(&J.counters[1], (unsigned long long)exec_blocks);
     atomicAdd(&J.counters[2], (unsigned long long)pruned_blocks);
@@ -603,31 +661,37 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
 }
 
 // FINAL kernels also serve passes that want their final rows (split mode): the
-// last item of such a pass runs the FINAL strip code.
-template <int R, bool WILD, bool FINAL>
+// last item of such a pass runs the FINAL strip code.  (A lambda here is not
+// always inlined; an outlined strip body addresses shared memory generically.)
+template <int R, bool WILD, bool FINAL, int BLK>
+__device__ __forceinline__ void run_item_x2(const PassParams& P, long long item,
+                                            WarpSmemX2<BLK>* sm, const uint32_t* tw_s) {
+  int s = 0;
+  const int j = item_job(P, item, &s);
+  if (FINAL && P.jobs[j].want_final && s == P.jobs[j].nstrips - 1)
+    run_strip_x2<R, WILD, FINAL, BLK>(P, P.jobs[j], s, sm, tw_s);
+  else
+    run_strip_x2<R, WILD, false, BLK>(P, P.jobs[j], s, sm, tw_s);
+}
+
+template <int R, bool WILD, bool FINAL, int BLK>
 __global__ void __launch_bounds__(256, 1) pass_kernel_x2(const PassParams P) {
-  __shared__ WarpSmemX2 wsm[8];
-  __shared__ uint32_t tw_s[8];
-  __shared__ long long base_s;
+  // dynamic shared memory, x2_smem_bytes<BLK>(blockDim.x / 32) (launch_any)
+  extern __shared__ __align__(16) unsigned char x2_dyn[];
+  WarpSmemX2<BLK>* wsm = reinterpret_cast<WarpSmemX2<BLK>*>(x2_dyn);
+  uint32_t* tw_s = reinterpret_cast<uint32_t*>(wsm + (blockDim.x >> 5));
+  long long* base_s = reinterpret_cast<long long*>(tw_s + 8);
   if (threadIdx.x < 8) tw_s[threadIdx.x] = P.tlo[threadIdx.x];
   __syncthreads();
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  WarpSmemX2* sm = &wsm[warp];
-  auto run = [&](long long item) {
-    int s = 0;
-    const int j = item_job(P, item, &s);
-    if (FINAL && P.jobs[j].want_final && s == P.jobs[j].nstrips - 1)
-      run_strip_x2<R, WILD, FINAL>(P, P.jobs[j], s, sm, tw_s);
-    else
-      run_strip_x2<R, WILD, false>(P, P.jobs[j], s, sm, tw_s);
-  };
+  WarpSmemX2<BLK>* sm = &wsm[warp];
   if (P.group > 0) {
     const int w = (int)(blockDim.x >> 7);
     for (;;) {
-      if (threadIdx.x == 0) base_s = (long long)atomicAdd(P.claim, (unsigned long long)P.group);
+      if (threadIdx.x == 0) *base_s = (long long)atomicAdd(P.claim, (unsigned long long)P.group);
       __syncthreads();
-      const long long base = base_s;
+      const long long base = *base_s;
       __syncthreads();
       if (base >= P.total_items) break;
       long long item = base + (warp & 3) * w + (warp >> 2);
@@ -636,7 +700,7 @@ __global__ void __launch_bounds__(256, 1) pass_kernel_x2(const PassParams P) {
         const long long q = P.total_items - 1 - p;
         item = (warp >> 2) == 0 ? (p <= q ? p : P.total_items) : (p < q ? q : P.total_items);
       }
-      if (item < P.total_items) run(item);
+      if (item < P.total_items) run_item_x2<R, WILD, FINAL, BLK>(P, item, sm, tw_s);
     }
     return;
   }
@@ -645,7 +709,7 @@ __global__ void __launch_bounds__(256, 1) pass_kernel_x2(const PassParams P) {
     if (lane == 0) item = (long long)atomicAdd(P.claim, 1ULL);
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item >= P.total_items) break;
-    run(item);
+    run_item_x2<R, WILD, FINAL, BLK>(P, item, sm, tw_s);
   }
 }
 

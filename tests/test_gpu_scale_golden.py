@@ -56,17 +56,20 @@ def _opt(name, value):
     get_context(0).set_option(name, value)
 
 
-@pytest.mark.parametrize("x2", [1, 0])
+@pytest.mark.parametrize("x2,blk", [(1, 32), (1, 64), (0, 0)])
 @pytest.mark.parametrize("prune", [True, False])
-def test_c2_score_pass(c2, x2, prune):
+def test_c2_score_pass(c2, x2, blk, prune):
+    """Packed kernel with 32- and 64-step blocks (x2_blk), and the 32-bit kernel."""
     s1, s2, _, _ = c2
     g = GOLDEN["C2"]
     _opt("x2", x2)
+    _opt("x2_blk", blk)
     try:
         rep = {}
         r = swb.score_only(s1, s2, SCHEME, AlignConfig(prune=prune), report=rep)
     finally:
         _opt("x2", 1)
+        _opt("x2_blk", 0)
     assert (r.score, list(r.end)) == (g["score"], g["end"])
     assert rep["kernel"] == ("packed16x2" if x2 else "lane32")
 
@@ -101,6 +104,19 @@ def test_c2_row_slabs_concurrent(c2, nslabs, prune, share):
         assert max(pruned) == 0
 
 
+def test_c2_row_slabs_concurrent_blk64(c2):
+    """The slab boundary protocol with 64-step packed blocks."""
+    _, _, a, b = c2
+    g = GOLDEN["C2"]
+    _opt("x2_blk", 64)
+    try:
+        with Session(get_context(0), a, b, SCHEME) as S:
+            merged, res = run_slabs_concurrent(S, slab_partition(S.n1, 4, SLAB_STRIP_ROWS), True, True)
+    finally:
+        _opt("x2_blk", 0)
+    assert (merged[0], [merged[1] + 1, merged[2] + 1]) == (g["score"], g["end"])
+
+
 def test_shared_best_prunes_more(c2):
     """Slabs below the alignment's start prune with the whole pass's best when
     it is shared (swb_pass_desc.shared_best) and far less on their own."""
@@ -130,8 +146,23 @@ def test_window_align(name):
     _check_align(name)
 
 
-def test_c3_window_split2():
-    _check_align("C3w_split", AlignConfig(split=2))
+@pytest.mark.parametrize("blk", [0, 64])
+def test_c3_window_split2(blk):
+    """split=2's halves on the packed FINAL kernels, 64-step blocks forced too."""
+    _opt("x2_blk", blk)
+    try:
+        _check_align("C3w_split", AlignConfig(split=2))
+    finally:
+        _opt("x2_blk", 0)
+
+
+@pytest.mark.parametrize("name", ["C3w", "C5w"])
+def test_window_align_blk64(name):
+    _opt("x2_blk", 64)
+    try:
+        _check_align(name)
+    finally:
+        _opt("x2_blk", 0)
 
 
 @pytest.mark.parametrize("world", [2, 4, 8])

@@ -14,18 +14,25 @@ pytestmark = pytest.mark.gpu
 
 
 def _both(a, b, scheme, prune=True):
+    """[packed kernel, 32-bit kernel] (score, end); the packed kernel runs with
+    32- and 64-step blocks (x2_blk) and must agree with itself."""
     ctx = get_context(0)
     s1 = Sequence.from_codes("a", a, scheme.alphabet)
     s2 = Sequence.from_codes("b", b, scheme.alphabet)
     out = []
     default = ctx.get_option("x2")
-    for flag in (1, 0):
-        ctx.set_option("x2", flag)
-        rep = {}
-        r = swb.score_only(s1, s2, scheme, AlignConfig(prune=prune), report=rep)
-        out.append((r.score, tuple(r.end)))
-    ctx.set_option("x2", default)
-    return out
+    try:
+        for flag, blk in ((1, 32), (1, 64), (0, 0)):
+            ctx.set_option("x2", flag)
+            ctx.set_option("x2_blk", blk)
+            rep = {}
+            r = swb.score_only(s1, s2, scheme, AlignConfig(prune=prune), report=rep)
+            out.append((r.score, tuple(r.end)))
+    finally:
+        ctx.set_option("x2", default)
+        ctx.set_option("x2_blk", 0)
+    assert out[0] == out[1], ("x2_blk 32 vs 64", out)
+    return [out[0], out[2]]
 
 
 @pytest.mark.parametrize("seed,n1,n2,kind", [
@@ -84,7 +91,7 @@ def test_x2_invariant_to_shape(n, seed):
     b = mutate_codes(rng, a, 0.12)[:n]
     sc = dna_scheme()
     ctx = get_context(0)
-    saved = {k: ctx.get_option(k) for k in ("x2", "x2_R", "max_ctas_per_sm")}
+    saved = {k: ctx.get_option(k) for k in ("x2", "x2_R", "max_ctas_per_sm", "x2_blk")}
     s1 = Sequence.from_codes("a", a, sc.alphabet)
     s2 = Sequence.from_codes("b", b, sc.alphabet)
     res = set()
@@ -94,9 +101,11 @@ def test_x2_invariant_to_shape(n, seed):
             ctx.set_option("x2", x2)
             ctx.set_option("x2_R", R)
             ctx.set_option("max_ctas_per_sm", ctas)
-            for prune in (True, False):
-                r = swb.score_only(s1, s2, sc, AlignConfig(prune=prune))
-                res.add((r.score, tuple(r.end)))
+            for blk in ((32, 64) if x2 else (0,)):
+                ctx.set_option("x2_blk", blk)
+                for prune in (True, False):
+                    r = swb.score_only(s1, s2, sc, AlignConfig(prune=prune))
+                    res.add((r.score, tuple(r.end)))
     finally:
         for k, v in saved.items():
             ctx.set_option(k, v)
