@@ -69,6 +69,10 @@ constexpr int kTrackNone = 0;
 constexpr int kTrackMin = 1;
 constexpr int kTrackMax = 2;
 constexpr int kPadCode = 7;  // row code for padding rows (profile byte -128)
+// Progress counters of consecutive strips sit one 128-byte line apart: every
+// counter is polled by its consumer and released by its producer each block,
+// and 32 counters to a line made each line a shared hot spot in L2.
+constexpr int kProgStride = 32;
 
 struct JobDev {
   const uint8_t* rows;  // code of row i = rows[i * rstep]
@@ -85,7 +89,7 @@ struct JobDev {
   int32_t want_final;
   int64_t item_base;
   int2* buf[2];          // row buffers (hm, F), n2 entries each
-  int32_t* progress;     // per strip: columns < progress[s] of strip s are published
+  int32_t* progress;     // per strip (stride kProgStride): columns < progress of strip s are published
   int32_t* fin_h;        // final row H (DP columns 1..n2) or null
   int32_t* fin_f;
   int4* strip_res;       // per strip (score_m, i, j, has)
@@ -571,8 +575,8 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
   const int cb0 = cb;
   const int2* __restrict__ inbuf = J.buf[(s + 1) & 1];  // written by strip s-1
   int2* __restrict__ outbuf = J.buf[s & 1];
-  int32_t* my_progress = J.progress + SWB_IX(s, J.nstrips);
-  const int32_t* up_progress = s > 0 ? J.progress + (s - 1) : nullptr;
+  int32_t* my_progress = J.progress + (long long)SWB_IX(s, J.nstrips) * kProgStride;
+  const int32_t* up_progress = s > 0 ? J.progress + (long long)(s - 1) * kProgStride : nullptr;
   // multi-GPU row slab: strip 0 consumes the slab above (another GPU), the
   // last strip produces into the slab below (peer memory); sys-scope ordering
   const bool ext_in = (s == 0) && (J.ext_in != nullptr);
@@ -1068,10 +1072,11 @@ __device__ __noinline__ void run_strip(const PassParams& P, const JobDev& Jg, in
         const int hi = s0 + 1 < ce ? s0 + 1 : ce;
         if (hi > cb && known_prog2 < hi) {
           if (P.chain_wait) {
-            known_prog2 = wait_acquire(J.progress + SWB_IX(s - 2, J.nstrips), hi);
+            known_prog2 = wait_acquire(J.progress + (long long)SWB_IX(s - 2, J.nstrips) * kProgStride, hi);
           } else {
-            if (ld_relaxed(J.progress + (s - 2)) < hi) wait_progress(J.progress + (s - 2), hi);
-            known_prog2 = ld_acquire(J.progress + (s - 2));
+            const int32_t* p2 = J.progress + (long long)(s - 2) * kProgStride;
+            if (ld_relaxed(p2) < hi) wait_progress(p2, hi);
+            known_prog2 = ld_acquire(p2);
           }
         }
       }

@@ -203,7 +203,7 @@ static void swb_watchdog_dump(swb_ctx* ctx, const unsigned long long* d_claim, c
   int2* ha = reinterpret_cast<int2*>(h + 1 + n);
   unsigned long long* hd = h + 1 + 2 * n;
   cudaMemcpyAsync(hc, d_claim, 8, cudaMemcpyDeviceToHost, st);
-  cudaMemcpyAsync(hp, d_prog, 4 * n, cudaMemcpyDeviceToHost, st);
+  cudaMemcpy2DAsync(hp, 4, d_prog, 4 * kProgStride, 4, n, cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(ha, d_alive, 8 * n, cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(hd, d_sdbg, 64 * n, cudaMemcpyDeviceToHost, st);
   cudaStreamSynchronize(st);
@@ -361,7 +361,7 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
       total_strips += r.nstrips;
       total_cols += r.n2;
     }
-    size_t bytes = 256 * 8 + sizeof(JobDev) * nj + sizeof(int32_t) * total_strips +
+    size_t bytes = 256 * 8 + sizeof(JobDev) * nj + sizeof(int32_t) * kProgStride * total_strips +
                    sizeof(int2) * total_strips + 256 + sizeof(int32_t) * 32 * kTabStride + 256 +
                    sizeof(unsigned long long) * 5 * nj + sizeof(int32_t) * nj + 64 +
                    sizeof(int4) * total_strips + 24 * total_strips + sizeof(int2) * 2 * total_cols +
@@ -373,7 +373,7 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     JobDev* d_jobs = A.take<JobDev>(nj);
     // zeroed region
     size_t zero_begin = (A.off + 255) & ~(size_t)255;
-    int32_t* d_prog = A.take<int32_t>(total_strips);
+    int32_t* d_prog = A.take<int32_t>(kProgStride * total_strips);
     unsigned long long* d_cnt = A.take<unsigned long long>(5 * nj);
     int32_t* d_pbest = A.take<int32_t>(nj);
     unsigned long long* d_claim = A.take<unsigned long long>(1);
@@ -455,7 +455,7 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
       J.item_base = item;
       J.buf[0] = A.take<int2>(r.n2);
       J.buf[1] = A.take<int2>(r.n2);
-      J.progress = d_prog + strip_off;
+      J.progress = d_prog + strip_off * kProgStride;
       J.strip_res = d_res + strip_off;
       J.strip_times = d_times + 3 * strip_off;
       J.counters = d_cnt + 5 * t;

@@ -122,8 +122,8 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
   const int rowB = R0 + 32 * R + lane * R;
   const int2* __restrict__ inbuf = J.buf[(s + 1) & 1];
   int2* __restrict__ outbuf = J.buf[s & 1];
-  int32_t* my_progress = J.progress + s;
-  const int32_t* up_progress = s > 0 ? J.progress + (s - 1) : nullptr;
+  int32_t* my_progress = J.progress + (long long)s * kProgStride;
+  const int32_t* up_progress = s > 0 ? J.progress + (long long)(s - 1) * kProgStride : nullptr;
   // multi-GPU row slab: item 0 consumes the slab above, the
   // last item produces into the slab below through peer memory (sys scope)
   const bool ext_in = (s == 0) && (J.ext_in != nullptr);
