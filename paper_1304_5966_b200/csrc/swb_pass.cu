@@ -568,11 +568,13 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     bool any_final_x2 = false;
     for (size_t t = g0; t < g1; ++t) any_final_x2 |= head.x2 && reqs[order[t]].want_final;
     // packed kernel block length: 64 steps (half the handoffs, releases and
-    // re-bases per column) for passes of more than one round of items; 32 for
-    // single-round passes, where the longer handoff lag and the longer
-    // optimistic re-runs cost more than they save
-    const int x2_blk = (ctx->x2_blk == 64 || (ctx->x2_blk == 0 && item > (long long)ctx->sms * 8))
-                           && x2_blk64_ok ? 64 : 32;
+    // re-bases per column) for a single pass of more than one round of items;
+    // 32 for single-round passes, where the longer handoff lag and the longer
+    // optimistic re-runs cost more than they save, and for launches of several
+    // passes (split=2's halves, row slabs), whose pruning the coarser blocks
+    // weaken
+    const bool auto64 = item > (long long)ctx->sms * 8 && g1 - g0 == 1;
+    const int x2_blk = (ctx->x2_blk == 64 || (ctx->x2_blk == 0 && auto64)) && x2_blk64_ok ? 64 : 32;
     if (head.x2) ctx->last_x2_blk = x2_blk;
     rc = head.x2  ? dispatch_x2(ctx, R, &P, item, ctas, nullptr, head.x2_wild, any_final_x2, x2_blk)
          : sc.big ? dispatch_big(ctx, R, &P, item, head.local, head.track, ctas, nullptr)
