@@ -107,7 +107,8 @@ int launch_any(swb_ctx* ctx, K kern, const PassParams& Pin, long long items, int
       // adjacent strips of one chain share a sub-partition: job-major order
       P.item_map = nullptr;
       P.group = 4 * per_sm;
-      P.mirror = (per_sm == 2 && items <= 8LL * ctx->sms && ctx->proto != 8) ? 1 : 0;
+      // pairs of items per sub-partition (swb_x2.cuh; the lane kernel mirrors)
+      P.mirror = (per_sm == 2 && items <= 8LL * ctx->sms && ctx->proto != 8) ? (ctx->proto == 12 ? 2 : 1) : 0;
       // dynamic shared memory pins the layout to exactly one CTA per SM
       const int pin = (int)std::max<size_t>(120 * 1024, dyn(threads));
       SWB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pin));

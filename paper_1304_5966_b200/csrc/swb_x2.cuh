@@ -695,7 +695,16 @@ __global__ void __launch_bounds__(256, 1) pass_kernel_x2(const PassParams P) {
       __syncthreads();
       if (base >= P.total_items) break;
       long long item = base + (warp & 3) * w + (warp >> 2);
-      if (P.mirror) {
+      // single round, two warps per sub-partition: items p and p + half share
+      // one, so the two reach their diagonals (tracked blocks on the pass's
+      // critical chain) half a pass apart (C2: 242 -> 232 ms against the
+      // mirrored pairs (p, last - p), kept as proto 12; unrelated +1.5 %)
+      if (P.mirror == 1) {
+        const long long half = (P.total_items + 1) / 2;
+        const long long p = base / 2 + (warp & 3);
+        const long long q = p + half;
+        item = (warp >> 2) == 0 ? (p < half ? p : P.total_items) : (q < P.total_items ? q : P.total_items);
+      } else if (P.mirror) {
         const long long p = base / 2 + (warp & 3);
         const long long q = P.total_items - 1 - p;
         item = (warp >> 2) == 0 ? (p <= q ? p : P.total_items) : (p < q ? q : P.total_items);
