@@ -48,6 +48,7 @@ int chk_take_other(long long* out);
 int chk_take_track(long long* out);
 int chk_take_big(long long* out);
 int chk_take_x2(long long* out);
+int chk_take_x2w(long long* out);
 
 #ifdef SWB_CHECKED
 #define SWB_CHK_TAKE(name)                                                          \

@@ -59,6 +59,8 @@ int dispatch_x2(swb_ctx* ctx, int R, const PassParams* P, long long items, int c
 }
 
 SWB_CHK_TAKE(chk_take_x2)
+#else
+SWB_CHK_TAKE(chk_take_x2w)
 #endif
 
 }  // namespace swb

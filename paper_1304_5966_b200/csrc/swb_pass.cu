@@ -622,7 +622,7 @@ int swb_run_passes(swb_ctx* ctx, const SchemeInt& sc, std::vector<PassReq>& reqs
     {
       long long chk[4];
       int (*takes[])(long long*) = {chk_take_local, chk_take_other, chk_take_track, chk_take_big,
-                                    chk_take_x2};
+                                    chk_take_x2, chk_take_x2w};
       for (auto take : takes) {
         if (take(chk) == 0 && chk[0])
           return swb_fail(SWB_ECUDA,
