@@ -244,8 +244,9 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     constexpr int MODE = decltype(trk_tag)::value;  // 0 untracked, 1 keys, 2 optimistic (= 0 here)
     constexpr bool TRK = MODE == 1;
     const int colA = st - lane, colB = colA - 32;
-    const int2 tp = sm->tz[tz_off + k];
-    const uint32_t tl = sm->prof[64 - lane + k], th = sm->prof[32 - lane + k];
+    const int2 tp = sm->tz[SWB_IX(tz_off + k, 2 * BLK)];
+    const uint32_t tl = sm->prof[SWB_IX(64 - lane + k, BLK + 64)],
+                   th = sm->prof[SWB_IX(32 - lane + k, BLK + 64)];
     const uint32_t up_h =
         (uint32_t)imad((int)__shfl_sync(0xffffffffu, out_hm, src_lane), up_mul, tp.x);
     const uint32_t up_f =
@@ -255,7 +256,7 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     if (guard && !actA && !actB) {
 #pragma unroll
       for (int r = 0; r < R; ++r) Hout[r] = Hin[r];
-      if (TRK) sm->trk[k & 31][lane] = bk2;
+      if (TRK) sm->trk[SWB_IX(k & 31, 32)][lane] = bk2;
       return;
     }
     const uint32_t keep = guard ? ((actA ? 0u : 0xffffu) | (actB ? 0u : 0xffff0000u)) : 0u;
@@ -294,15 +295,15 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     out_f = fv;
     if (TRK) {
       bk2 = guard ? vimax3_2(bk2, cm & ~keep, 0u) : cm;
-      sm->trk[k & 31][lane] = bk2;
+      sm->trk[SWB_IX(k & 31, 32)][lane] = bk2;
     }
-    if (lane == 31 && actB) sm->out[k] = make_uint2(out_hm, out_f);
+    if (lane == 31 && actB) sm->out[SWB_IX(k, BLK)] = make_uint2(out_hm, out_f);
     if (FINAL && lane == lstar) {
       const int col = hstar ? colB : colA;
       if (col >= 0 && col < n2) {
         const int off = base - kX2Off;
-        J.fin_h[col] = (hstar ? hi16(fh) : lo16(fh)) + off + goe;
-        J.fin_f[col] = (hstar ? hi16(ff) : lo16(ff)) + off;
+        J.fin_h[SWB_IX(col, n2)] = (hstar ? hi16(fh) : lo16(fh)) + off + goe;
+        J.fin_f[SWB_IX(col, n2)] = (hstar ? hi16(ff) : lo16(ff)) + off;
       }
     }
   };
@@ -330,7 +331,7 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
       for (int h = 0; h < NH; ++h) {
         code[h] = code_next[h];
         const int cn = s0 + kX2Blk + 32 * h + lane;
-        code_next[h] = (cn < n2) ? (int)J.cols[(long long)cn * J.cstep] : 0;
+        code_next[h] = (cn < n2) ? (int)J.cols[SWB_IX((long long)cn * J.cstep, (long long)n2 * J.cstep)] : 0;
       }
       if (has_top && s0 < n2) {
         const int need = (s0 + kX2Blk < n2) ? s0 + kX2Blk : n2;
@@ -354,19 +355,20 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
       for (int h = 0; h < NH; ++h) {
         const int c = s0 + 32 * h + lane;
         if (has_top && c < n2) {
-          const int2 v = __ldcg(inbuf + c);
+          const int2 v = __ldcg(inbuf + SWB_IX(c, n2));
           top_h[h] = v.x;
           top_f[h] = v.y;
         }
       }
       // keep the window's last 64 columns, then the block's new ones
-      const uint32_t p1 = sm->prof[kX2Blk + lane], p2 = sm->prof[kX2Blk + 32 + lane];
+      const uint32_t p1 = sm->prof[SWB_IX(kX2Blk + lane, BLK + 64)],
+                     p2 = sm->prof[SWB_IX(kX2Blk + 32 + lane, BLK + 64)];
       __syncwarp();
       sm->prof[lane] = p1;
       sm->prof[32 + lane] = p2;
 #pragma unroll
       for (int h = 0; h < NH; ++h)
-        sm->prof[64 + 32 * h + lane] = s0 + 32 * h + lane < n2 ? tw_s[code[h]] : 0u;
+        sm->prof[SWB_IX(64 + 32 * h + lane, BLK + 64)] = s0 + 32 * h + lane < n2 ? tw_s[SWB_IX(code[h], 8)] : 0u;
     }
 
     // (1b) re-base: warp maximum over the state and the incoming top row
@@ -406,7 +408,7 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     // the producer's row in this block's frame (lane 0 injects it at step k)
 #pragma unroll
     for (int h = 0; h < NH; ++h)
-      sm->tz[32 * h + lane] = make_int2(clamp_rel((long long)top_h[h] - base + kX2Off),
+      sm->tz[SWB_IX(32 * h + lane, 2 * BLK)] = make_int2(clamp_rel((long long)top_h[h] - base + kX2Off),
                                         clamp_rel((long long)top_f[h] - base + kX2Off));
     __syncwarp();
     const bool steady = (s0 >= 63) && (s0 + kX2Blk <= n2);
@@ -515,7 +517,7 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
             int lo = 0;
 #pragma unroll
             for (int stp = 16; stp > 0; stp >>= 1) {
-              const uint32_t w = sm->trk[lo + stp - 1][lane];
+              const uint32_t w = sm->trk[SWB_IX(lo + stp - 1, 32)][lane];
               if ((hiHalf ? hi16(w) : lo16(w)) < key) lo += stp;
             }
             v = (int)(vref + (key >> 5) - 1);
@@ -575,11 +577,11 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
         if (cf >= 0 && cf < n2) {
           int2 o = make_int2(-goe, SWB_NEG32);  // pruned block: the fill values
           if (!skip) {
-            const uint2 raw = sm->out[32 * h + lane];
+            const uint2 raw = sm->out[SWB_IX(32 * h + lane, BLK)];
             const int off = base - kX2Off;
             o = make_int2(hi16(raw.x) + off, hi16(raw.y) + off);
           }
-          __stcg(outbuf + cf, o);
+          __stcg(outbuf + SWB_IX(cf, n2), o);
         }
       }
       if (ext_out) __threadfence_system();
