@@ -267,7 +267,11 @@ int32_t swb_measure_int_peak(swb_ctx* ctx, swb_int_peak* out);
  * (0 auto, 1 CTA claiming, 2 warp claiming), "proto", "reset_debug",
  * "job_major", "bound_maps", "live_ranges", "p2_R", "mm_R", "mm_static",
  * "mm_dyn", "chain_wait" (acquire polling in chain-shaped passes),
- * "chain_cta" (chain-shaped passes in CTA chunks of 4 strips). */
+ * "chain_cta" (chain-shaped passes in CTA chunks),
+ * "chain_chunk" (4 or 8 strips per chunk), "x2_blk" (packed kernel steps per
+ * block: 0 = by rounds of items, 32, 64), "map_tile_log2",
+ * "wide_log2" (int64-kernel threshold, §3.11), "watchdog_ms", "claim_log",
+ * "min_R", "live_big". */
 int32_t swb_set_option(swb_ctx* ctx, const char* name, int64_t value);
 /* Current value of a tuning option (-1 for an unknown name). */
 int64_t swb_get_option(swb_ctx* ctx, const char* name);
