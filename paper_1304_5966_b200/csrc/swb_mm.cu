@@ -136,6 +136,110 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineDev* subs, Co
   }
 }
 
+// Chunked combine: the top Myers-Miller levels have few subproblems of
+// millions of columns, which one CTA each scanned at a single SM's bandwidth
+// (C3: 130 ms over the levels).  Each CTA now reduces kCombChunk columns of one
+// subproblem to (max hh, first j) and (max ff, first j); one warp per
+// subproblem merges its chunks and applies combine_kernel's rule.
+constexpr int kCombChunk = 16384;
+
+struct CombArena {  // 256-byte aligned carving of one scratch allocation
+  char* base = nullptr;
+  size_t off = 0;
+  template <typename T>
+  T* take(size_t count) {
+    off = (off + 255) & ~(size_t)255;
+    T* p = reinterpret_cast<T*>(base + off);
+    off += sizeof(T) * (count > 0 ? count : 1);
+    return p;
+  }
+};
+
+struct CombinePart {
+  long long mh, mf;
+  int jh, jf;
+};
+
+// (m, j) pairs: larger m wins, equal m -> smaller j
+__device__ inline void take_first_max(long long& m, int& j, long long om, int oj) {
+  if (om > m || (om == m && oj < j)) {
+    m = om;
+    j = oj;
+  }
+}
+
+__global__ void __launch_bounds__(256) combine_part_kernel(const CombineDev* subs,
+                                                           const int* chunk_sub,
+                                                           const int* chunk_lo,
+                                                           CombinePart* parts, int go, int ge) {
+  const CombineDev c = subs[chunk_sub[blockIdx.x]];
+  const int lo = chunk_lo[blockIdx.x];
+  const int hi = min(lo + kCombChunk, c.cols + 1);
+  const int cols = c.cols;
+  long long mh = LLONG_MIN, mf = LLONG_MIN;
+  int jh = INT_MAX, jf = INT_MAX;
+  for (int j = lo + threadIdx.x; j < hi; j += blockDim.x) {  // increasing j: strict > keeps the first
+    const long long hh = up_h(c, j, go, ge) + dn_h(c, cols - j, go, ge);
+    const long long ff = up_f(c, j, go, ge) + dn_f(c, cols - j, go, ge) + go;
+    if (hh > mh) { mh = hh; jh = j; }
+    if (ff > mf) { mf = ff; jf = j; }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    take_first_max(mh, jh, __shfl_down_sync(0xffffffffu, mh, o), __shfl_down_sync(0xffffffffu, jh, o));
+    take_first_max(mf, jf, __shfl_down_sync(0xffffffffu, mf, o), __shfl_down_sync(0xffffffffu, jf, o));
+  }
+  __shared__ CombinePart w[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) w[warp] = CombinePart{mh, mf, jh, jf};
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    CombinePart r = w[0];
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+      take_first_max(r.mh, r.jh, w[k].mh, w[k].jh);
+      take_first_max(r.mf, r.jf, w[k].mf, w[k].jf);
+    }
+    parts[blockIdx.x] = r;
+  }
+}
+
+__global__ void __launch_bounds__(256) combine_final_kernel(const CombineDev* subs, int n,
+                                                            const int* part_off,
+                                                            const CombinePart* parts,
+                                                            CombineOut* out, int go, int ge) {
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= n) return;
+  long long mh = LLONG_MIN, mf = LLONG_MIN;
+  int jh = INT_MAX, jf = INT_MAX;
+  for (int q = part_off[t] + lane; q < part_off[t + 1]; q += 32) {
+    take_first_max(mh, jh, parts[q].mh, parts[q].jh);
+    take_first_max(mf, jf, parts[q].mf, parts[q].jf);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    take_first_max(mh, jh, __shfl_down_sync(0xffffffffu, mh, o), __shfl_down_sync(0xffffffffu, jh, o));
+    take_first_max(mf, jf, __shfl_down_sync(0xffffffffu, mf, o), __shfl_down_sync(0xffffffffu, jf, o));
+  }
+  if (lane == 0) {
+    const CombineDev c = subs[t];
+    const long long best = max(mh, mf);
+    const long long h = mh == best ? jh : LLONG_MAX, f = mf == best ? jf : LLONG_MAX;
+    CombineOut o;
+    o.best = best;
+    o.gap = !(h <= f);  // plain join wins ties at equal column
+    o.j = o.gap ? f : h;
+    const int j = (int)o.j;
+    if (o.gap) {
+      o.upper = up_f(c, j, go, ge);
+      o.lower = dn_f(c, c.cols - j, go, ge);
+    } else {
+      o.upper = up_h(c, j, go, ge);
+      o.lower = dn_h(c, c.cols - j, go, ge);
+    }
+    o.status = best == c.expected ? 0 : 1;
+    out[t] = o;
+  }
+}
+
 // ---- leaves -------------------------------------------------------------------
 
 struct LeafDev {
@@ -479,15 +583,47 @@ extern "C" int32_t swb_crossings(swb_ctx* ctx, const swb_scheme* scheme, int32_t
   for (auto& r : reqs) cells += r.cells;
   if (cells_out) *cells_out = cells;
 
-  CombineDev* d_comb = (CombineDev*)swb_scratch(ctx->misc, sizeof(CombineDev) * n +
-                                                                sizeof(CombineOut) * n + 512);
-  if (!d_comb) return swb_fail(SWB_ECUDA, "out of device memory");
-  CombineOut* d_out = reinterpret_cast<CombineOut*>(
-      (reinterpret_cast<uintptr_t>(d_comb + n) + 255) & ~(uintptr_t)255);
+  // chunks of kCombChunk columns: (subproblem, first column) per chunk, and
+  // each subproblem's first chunk
+  std::vector<int> chunk_sub, chunk_lo, part_off(n + 1, 0);
+  for (int t = 0; t < n; ++t) {
+    part_off[t] = (int)chunk_sub.size();
+    for (long long lo = 0; lo <= comb[t].cols; lo += kCombChunk) {
+      chunk_sub.push_back(t);
+      chunk_lo.push_back((int)lo);
+    }
+  }
+  part_off[n] = (int)chunk_sub.size();
+  const size_t nch = chunk_sub.size();
+  CombArena CA;
+  CA.base = (char*)swb_scratch(ctx->misc, sizeof(CombineDev) * n + sizeof(CombineOut) * n +
+                                              sizeof(int) * (2 * nch + n + 1) +
+                                              sizeof(CombinePart) * nch + 6 * 256);
+  if (!CA.base) return swb_fail(SWB_ECUDA, "out of device memory");
+  CombineDev* d_comb = CA.take<CombineDev>(n);
+  CombineOut* d_out = CA.take<CombineOut>(n);
+  int* d_csub = CA.take<int>(nch);
+  int* d_clo = CA.take<int>(nch);
+  int* d_poff = CA.take<int>(n + 1);
+  CombinePart* d_parts = CA.take<CombinePart>(nch);
   SWB_CUDA(cudaMemcpyAsync(d_comb, comb.data(), sizeof(CombineDev) * n, cudaMemcpyHostToDevice,
                            ctx->stream));
-  combine_kernel<<<n, 256, 0, ctx->stream>>>(d_comb, d_out, sc.go, sc.ge);
-  ctx->launches++;
+  SWB_CUDA(cudaMemcpyAsync(d_csub, chunk_sub.data(), sizeof(int) * nch, cudaMemcpyHostToDevice,
+                           ctx->stream));
+  SWB_CUDA(cudaMemcpyAsync(d_clo, chunk_lo.data(), sizeof(int) * nch, cudaMemcpyHostToDevice,
+                           ctx->stream));
+  SWB_CUDA(cudaMemcpyAsync(d_poff, part_off.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice,
+                           ctx->stream));
+  if (ctx->proto == 15) {  // the one-CTA-per-subproblem combine (A/B)
+    combine_kernel<<<n, 256, 0, ctx->stream>>>(d_comb, d_out, sc.go, sc.ge);
+    ctx->launches++;
+  } else {
+    combine_part_kernel<<<(unsigned)nch, 256, 0, ctx->stream>>>(d_comb, d_csub, d_clo, d_parts,
+                                                                sc.go, sc.ge);
+    combine_final_kernel<<<(n + 7) / 8, 256, 0, ctx->stream>>>(d_comb, n, d_poff, d_parts, d_out,
+                                                               sc.go, sc.ge);
+    ctx->launches += 2;
+  }
   SWB_CUDA(cudaGetLastError());
   std::vector<CombineOut> h(n);
   SWB_CUDA(cudaMemcpyAsync(h.data(), d_out, sizeof(CombineOut) * n, cudaMemcpyDeviceToHost,
