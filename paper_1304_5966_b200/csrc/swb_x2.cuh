@@ -308,6 +308,13 @@ __device__ __forceinline__ void run_strip_x2(const PassParams& P, const JobDev& 
     }
   };
 
+  // Diagnostics (proto 16 / 17): start the item only once its producer leads
+  // by 96 / 160 columns, i.e. with more slack in the chain (C2 -0.7 %,
+  // unrelated +2 / +6 %: off by default)
+  if ((P.proto == 16 || P.proto == 17) && has_top) {
+    const int lead = P.proto == 16 ? 96 : 160;
+    wait_progress(up_progress, lead < n2 ? lead : n2, ext_in);
+  }
   for (int s0 = 0; s0 < s_end; s0 += kX2Blk) {
     // (1) wait for and read the producer's bottom row for [s0, s0 + BLK); shift
     //     the profile window and stage the new columns' words
